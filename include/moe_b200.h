@@ -1,0 +1,234 @@
+/*
+ * moe_b200.h — C ABI of the B200-native MegaScale-MoE layer hot path.
+ *
+ * One entry per operator of the reference's operator vocabulary
+ * (OpKind, /root/reference/proj/core/include/moeplan/simsched.hpp:32-44;
+ * node names, core/src/graph.cpp:254-311) plus the routing-map functions the
+ * reference implements on the CPU (core/include/moeplan/routing.hpp:49-106)
+ * and the FP8 communication quantiser (numerics.hpp:61-62). Each declaration
+ * names the reference interface it replaces.
+ *
+ * Conventions
+ *   - plain pointers + explicit sizes; "d_" = device pointer, "h_" = host;
+ *     no C++ or torch types cross this boundary.
+ *   - every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) unless stated otherwise; no call synchronises the device.
+ *   - index widths: token/row ids int32 on device (T*k < 2^31 at every
+ *     BASELINE config); the C++ compat adapter widens to long long.
+ *   - bf16 tensors are passed as uint16_t* (raw bits), row-major.
+ *   - errors: a status code, never an exception (reference: domain_error ->
+ *     exit 2, other -> 1, tools/src/main.cpp:595-604); moe_last_error() gives
+ *     the message of the last failure on the calling thread.
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MOE_OK = 0,
+    MOE_ERR_INTERNAL = 1,    /* reference: other std::exception -> exit 1 */
+    MOE_ERR_INVALID = 2,     /* reference: std::domain_error -> exit 2 */
+    MOE_ERR_CUDA = 3,
+    MOE_ERR_TIMEOUT = 4,     /* cross-GPU flag wait exceeded its bound */
+    MOE_ERR_UNSUPPORTED = 5
+} moe_status;
+
+typedef void* moe_stream_t; /* cudaStream_t */
+
+const char* moe_last_error(void);
+int moe_version(void);
+/* Number of kernel launches this library issued on the calling process
+ * since the last reset (evidence counter for bench gpu_launches). */
+uint64_t moe_launch_count(void);
+void moe_launch_count_reset(void);
+
+/* ===================================================================== */
+/* Routing maps (integer, bit-exact with the reference)                   */
+/* ===================================================================== */
+
+/* Group-capacity token drop.
+ * Replaces: routing.cpp:113-131 (tail of simulate_routing).
+ * capacity = ceil(cf * T * k / n_groups) computed in double on the host
+ * exactly as routing.cpp:115-117; tokens are dropped whole, highest index
+ * first, while any of their groups is over capacity.
+ * d_experts[T*k] int32, d_dropped[T] uint8 out. Workspace: none. */
+moe_status moe_capacity_drop(const int32_t* d_experts, int64_t T, int64_t E, int64_t k,
+                             int64_t n_groups, double capacity_factor, uint8_t* d_dropped,
+                             moe_stream_t stream);
+
+/* Bytes of device workspace moe_permute needs for T tokens. */
+size_t moe_permute_workspace_size(int64_t T, int64_t E, int64_t k, int64_t n_src);
+
+/* Local-scatter row map for `my_rank`.
+ * Replaces: routing::build_scatter_map (routing.hpp:72, routing.cpp:135-187).
+ * Inputs: d_experts[T*k], d_source_rank[T] (values in [0, n_src)),
+ *         d_dropped[T] (may be NULL = none dropped).
+ * Outputs (capacity T*k rows; *h_rows/d_rows = retained local rows):
+ *   d_row_map_in[rows]     = t*k + slot, ordered by (expert, source_rank, t)
+ *   d_per_expert_counts[E] = retained (t,slot) per expert over ALL experts
+ *   d_out_expert[rows], d_out_source_rank[rows]
+ *   d_expert_offsets[E/n+1] unpadded row offsets of the local experts
+ * (row_map_out is the identity and inverse_map == row_map_in in the
+ * reference, routing.cpp:179-181; the adapter materialises them.)
+ * Errors: MOE_ERR_INVALID unless n >= 1, 0 <= my_rank < n, E % n == 0
+ * (routing.cpp:136-138). */
+moe_status moe_permute(const int32_t* d_experts, const int32_t* d_source_rank,
+                       const uint8_t* d_dropped, int64_t T, int64_t E, int64_t k, int64_t n,
+                       int64_t my_rank, int64_t n_src, int32_t* d_row_map_in,
+                       int32_t* d_per_expert_counts, int32_t* d_out_expert,
+                       int32_t* d_out_source_rank, int32_t* d_expert_offsets,
+                       int32_t* d_rows, void* d_workspace, moe_stream_t stream);
+
+/* Tile slicing with per-tile dependent-source-rank sets.
+ * Replaces: routing::sort_tokens_for_tiles (routing.hpp:88-89,
+ * routing.cpp:189-217). Dependent ranks returned as a bitmask (ranks < 64)
+ * plus the [lo, hi] window the fused dispatch waits on.
+ * d_expert_offsets from moe_permute; outputs sized >= rows + E/n tiles.
+ * *d_num_tiles (device) receives the tile count. */
+moe_status moe_tile_layout(const int32_t* d_out_source_rank, const int32_t* d_expert_offsets,
+                           int64_t num_local_experts, int64_t first_expert, int64_t tile_rows,
+                           int32_t* d_tile_expert, int32_t* d_tile_begin, int32_t* d_tile_end,
+                           uint64_t* d_tile_rank_mask, int32_t* d_num_tiles,
+                           moe_stream_t stream);
+
+/* Integer part of routing::balance_metrics (routing.hpp:101,
+ * routing.cpp:219-262): d_per_group_load[n] (retained slots),
+ * d_assigned[n] (all slots), d_dropped_tokens[1]. The host finishes the
+ * double arithmetic exactly as the reference does (see the C++ adapter). */
+moe_status moe_balance_counts(const int32_t* d_experts, const uint8_t* d_dropped, int64_t T,
+                              int64_t E, int64_t k, int64_t n, int64_t* d_per_group_load,
+                              int64_t* d_assigned, int64_t* d_dropped_tokens,
+                              moe_stream_t stream);
+
+/* ===================================================================== */
+/* Router (reference node `router`, graph.cpp:268-271; cost only there)   */
+/* ===================================================================== */
+
+/* logits[T,E] = x[T,h] . wr[E,h]^T (bf16 in, fp32 accumulate); top-k by
+ * logit, ties -> lower expert id, slot 0 = largest; gates = softmax over
+ * the k selected logits. d_logits may be NULL. */
+moe_status moe_router_topk(const uint16_t* d_x, const uint16_t* d_wr, int64_t T, int64_t h,
+                           int64_t E, int64_t k, float* d_logits, int32_t* d_experts,
+                           float* d_gates, moe_stream_t stream);
+
+/* Top-k + gate softmax from given fp32 logits (bit-exact selection). */
+moe_status moe_topk_from_logits(const float* d_logits, int64_t T, int64_t E, int64_t k,
+                                int32_t* d_experts, float* d_gates, moe_stream_t stream);
+
+/* ===================================================================== */
+/* FP8 communication (numerics.hpp:43-62)           */
+/* ===================================================================== */
+
+/* Per-row (per_token, 1 x h) E4M3 quantisation: scale = absmax/448 (1 for
+ * an all-zero row), codes = RNE(x/scale) saturating at 448.
+ * Replaces: numerics::quantize(..., per_token, fp8_e4m3) for the data path.
+ * x bf16 [rows, cols]; codes e4m3 bytes [rows, cols]; scales fp32 [rows]. */
+moe_status moe_quantize_e4m3_rows(const uint16_t* d_x, int64_t rows, int64_t cols,
+                                  uint8_t* d_codes, float* d_scales, moe_stream_t stream);
+/* fp32-input variant (bit-exact against the reference's quantize on
+ * fp32-representable inputs). */
+moe_status moe_quantize_e4m3_rows_f32(const float* d_x, int64_t rows, int64_t cols,
+                                      uint8_t* d_codes, float* d_scales, moe_stream_t stream);
+
+/* ===================================================================== */
+/* MoE layer (router -> dispatch -> fc1/SwiGLU -> fc2 -> combine)          */
+/* ===================================================================== */
+
+typedef struct moe_layer moe_layer; /* opaque */
+
+typedef enum { MOE_GATE_BEFORE_FC2 = 0, MOE_GATE_AFTER_FC2 = 1 } moe_gate_order; /* numerics.hpp:86 */
+typedef enum { MOE_COMM_BF16 = 0, MOE_COMM_FP8 = 1 } moe_comm_format;           /* config.hpp:41 */
+typedef enum { MOE_EP_AG_RS = 0, MOE_EP_A2A = 1 } moe_ep_pattern;               /* commcost.hpp:81 */
+
+typedef struct {
+    int64_t tokens_per_rank; /* T_r (b*s/n, graph.cpp:111-113) */
+    int64_t hidden;          /* h */
+    int64_t ffn_hidden;      /* f (per expert) */
+    int64_t num_experts;     /* E */
+    int64_t top_k;           /* k */
+    int64_t ep_size;         /* n (ranks) */
+    int64_t rank;            /* this rank */
+    double capacity_factor;  /* <= 0: no drop */
+    int32_t gate_order;      /* moe_gate_order */
+    int32_t comm_format;     /* moe_comm_format */
+    int32_t ep_pattern;      /* moe_ep_pattern */
+    int32_t route_mode;      /* 0 = learned router (K1), 1 = injected experts/gates */
+} moe_layer_config;
+
+moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out);
+void moe_layer_destroy(moe_layer* L);
+
+/* Weights in the reference layout: w1 [E_local][2f][h] with rows [0,f) = a
+ * and [f,2f) = b (SwiGLU = a * silu(b), numerics.cpp:262-268); w2
+ * [E_local][h][f]; wr [E][h] (router, replicated). Copied into the layer's
+ * HBM layout (w1 interleaved per 128-row a/b block for the fused epilogue). */
+moe_status moe_layer_set_weights(moe_layer* L, const uint16_t* d_w1, const uint16_t* d_w2,
+                                 const uint16_t* d_wr, moe_stream_t stream);
+
+/* Device pointer of the layer's symmetric input buffer [T_r, h] bf16. A
+ * caller may write x there directly and pass NULL as d_x to forward. */
+uint16_t* moe_layer_input_buffer(moe_layer* L);
+
+/* Injected routing (route_mode = 1): experts [T_r, k] int32, gates [T_r, k]
+ * fp32 for this rank's tokens. */
+moe_status moe_layer_set_routing(moe_layer* L, const int32_t* d_experts, const float* d_gates,
+                                 moe_stream_t stream);
+
+/* Forward: y[T_r, h] = MoE(x). Retains what backward needs (fc1_out,
+ * routing maps). Collective when ep_size > 1. */
+moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y,
+                             moe_stream_t stream);
+
+/* Backward: dx[T_r, h] from dy[T_r, h]; weight gradients written (not
+ * accumulated) into dw1 [E_local][2f][h] (reference layout), dw2
+ * [E_local][h][f], dwr [E][h] (fp32, this rank's tokens' contribution).
+ * Any gradient pointer may be NULL to skip it. */
+moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx,
+                              uint16_t* d_dw1, uint16_t* d_dw2, float* d_dwr,
+                              moe_stream_t stream);
+
+/* Routing results of the last forward (device pointers owned by the layer):
+ * experts/gates [T_global, k], dropped [T_global], row_map_in [rows],
+ * per_expert_counts [E], out_expert/out_source_rank [rows], rows (device). */
+typedef struct {
+    const int32_t* experts;
+    const float* gates;
+    const uint8_t* dropped;
+    const int32_t* row_map_in;
+    const int32_t* per_expert_counts;
+    const int32_t* out_expert;
+    const int32_t* out_source_rank;
+    const int32_t* rows;
+    const float* dgates; /* after backward: [T_r, k] */
+    const float* logits; /* learned-router mode: [T_r, E] */
+} moe_layer_routing_view;
+moe_status moe_layer_routing(moe_layer* L, moe_layer_routing_view* view);
+
+/* Per-phase device timings of the last forward/backward (ms), measured with
+ * CUDA events on the layer stream when timing is enabled. */
+moe_status moe_layer_enable_timing(moe_layer* L, int enable);
+moe_status moe_layer_phase_times(moe_layer* L, float* h_ms, int max_phases, int* n_phases,
+                                 const char** names);
+
+/* ===================================================================== */
+/* Multi-GPU fabric (NVLink P2P over NVSwitch; one process per GPU)       */
+/* ===================================================================== */
+
+/* Size of this rank's IPC export blob. */
+size_t moe_layer_ipc_handle_size(void);
+/* Export the handle of this rank's symmetric buffers (host bytes). */
+moe_status moe_layer_ipc_export(moe_layer* L, void* h_blob);
+/* Import all ranks' blobs (n * moe_layer_ipc_handle_size() bytes, rank
+ * order) and map peer buffers. Call once after every rank exported. */
+moe_status moe_layer_ipc_import(moe_layer* L, const void* h_blobs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_B200_H */

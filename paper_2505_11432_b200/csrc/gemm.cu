@@ -1,0 +1,109 @@
+// gemm.cu — host launchers for the tcgen05 grouped GEMM (gemm_sm100.cuh)
+// and the C-ABI `moe_grouped_gemm` operator (reference OpKind::grouped_gemm,
+// simsched.hpp:32-44).
+#include "gemm.h"
+
+namespace moe {
+
+template <int BN, bool A_MN, bool B_MN, bool KG, int EPI>
+static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                              int grid, cudaStream_t s) {
+    using Cfg = GemmCfg<BN>;
+    auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, KG, EPI>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          Cfg::SMEM_BYTES));
+        attr_set = true;
+    }
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(ta, tb, a);
+    count_launch();
+    MOE_CUDA_TRY(cudaGetLastError());
+    return MOE_OK;
+}
+
+moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s) {
+    MOE_CHECK_ARG(a.G >= 1 && a.G <= GemmCfg<256>::MAX_GROUPS, "grouped GEMM: 1 <= groups <= 256");
+    const int grid = p.grid > 0 ? p.grid : kNumSMs;
+#define MOE_GEMM_CASE(BN, AMN, BMN, KG, EPI)                                               \
+    if (p.bn == BN && p.a_mn == AMN && p.b_mn == BMN && p.k_grouped == KG && p.epi == EPI) \
+        return launch_impl<BN, AMN, BMN, KG, EPI>(p.ta, p.tb, a, grid, s);
+    // forward fc1 (fused SwiGLU) / fc2 (scatter to combine staging)
+    MOE_GEMM_CASE(256, false, false, false, EPI_SWIGLU)
+    MOE_GEMM_CASE(256, false, false, false, EPI_SCATTER)
+    // dgrads: weights read MN-major
+    MOE_GEMM_CASE(256, false, true, false, EPI_SWIGLU_BWD)
+    MOE_GEMM_CASE(256, false, true, false, EPI_SCATTER)
+    // wgrads
+    MOE_GEMM_CASE(256, true, true, true, EPI_STORE_BF16)
+    MOE_GEMM_CASE(256, true, true, true, EPI_STORE_F32)
+    // generic (tests / attention projections)
+    MOE_GEMM_CASE(256, false, false, false, EPI_STORE_BF16)
+    MOE_GEMM_CASE(256, false, false, false, EPI_STORE_F32)
+    MOE_GEMM_CASE(256, false, true, false, EPI_STORE_BF16)
+    MOE_GEMM_CASE(256, false, true, false, EPI_STORE_F32)
+    MOE_GEMM_CASE(128, false, false, false, EPI_STORE_BF16)
+    MOE_GEMM_CASE(128, false, false, false, EPI_STORE_F32)
+#undef MOE_GEMM_CASE
+    return set_error(MOE_ERR_UNSUPPORTED, "grouped GEMM variant not instantiated (bn=%d a_mn=%d b_mn=%d kg=%d epi=%d)",
+                     p.bn, (int)p.a_mn, (int)p.b_mn, (int)p.k_grouped, p.epi);
+}
+
+// Tensor maps for the operand layouts used by the kernel.
+moe_status tmap_kmajor(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box_rows) {
+    return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)K, (uint64_t)rows,
+                        (uint64_t)K * 2, 64, (uint32_t)box_rows);
+}
+
+moe_status tmap_mnmajor(CUtensorMap* m, const void* base, int64_t krows, int64_t mn) {
+    return make_tmap_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)mn, (uint64_t)krows,
+                        (uint64_t)mn * 2, 64, 64);
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b, void* d_d,
+                                       int32_t groups, const int32_t* d_group_rows,
+                                       int64_t total_rows, int64_t M, int64_t N, int64_t K,
+                                       int32_t a_mn_major, int32_t b_mn_major,
+                                       int32_t k_grouped, int32_t out_f32, int32_t bn,
+                                       moe_stream_t stream) {
+    MOE_CHECK_ARG(d_a && d_b && d_d && d_group_rows, "null pointer");
+    MOE_CHECK_ARG(bn == 128 || bn == 256, "bn must be 128 or 256");
+    MOE_CHECK_ARG(N % 64 == 0 && K % 64 == 0 && M % 128 == 0 || !k_grouped, "K-grouped: M%128, N%64, K%64");
+    GemmPlan p;
+    p.bn = bn;
+    p.a_mn = a_mn_major != 0;
+    p.b_mn = b_mn_major != 0;
+    p.k_grouped = k_grouped != 0;
+    p.epi = out_f32 ? EPI_STORE_F32 : EPI_STORE_BF16;
+    GemmArgs a{};
+    a.G = groups;
+    a.group_rows = d_group_rows;
+    a.N = (int)N;
+    a.out = d_d;
+    a.ldo = N;
+    if (!k_grouped) {
+        // A [total_rows, K] K-major; B: K-major [G*N, K] or MN-major [G*K, N]
+        MOE_CHECK_ARG(!a_mn_major, "M-grouped GEMM needs K-major A");
+        MOE_CHECK_ARG(K % 8 == 0 && N % 8 == 0, "K and N must be multiples of 8");
+        a.K = (int)K;
+        MOE_TRY(tmap_kmajor(&p.ta, d_a, total_rows, K, 128));
+        if (!b_mn_major) {
+            a.b_group_stride = (int)N;
+            MOE_TRY(tmap_kmajor(&p.tb, d_b, (int64_t)groups * N, K, bn));
+        } else {
+            a.b_group_stride = (int)K;
+            MOE_TRY(tmap_mnmajor(&p.tb, d_b, (int64_t)groups * K, N));
+        }
+    } else {
+        // A [total_rows, M] MN-major, B [total_rows, N] MN-major, D [G*M, N]
+        MOE_CHECK_ARG(a_mn_major && b_mn_major, "K-grouped GEMM needs MN-major A and B");
+        a.K = (int)M;
+        MOE_TRY(tmap_mnmajor(&p.ta, d_a, total_rows, M));
+        MOE_TRY(tmap_mnmajor(&p.tb, d_b, total_rows, N));
+    }
+    return gemm_launch(p, a, (cudaStream_t)stream);
+}

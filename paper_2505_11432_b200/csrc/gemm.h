@@ -1,0 +1,28 @@
+// gemm.h — host-side plan for the tcgen05 grouped GEMM.
+#pragma once
+
+#include "gemm_sm100.cuh"
+#include "runtime.h"
+
+namespace moe {
+
+struct GemmPlan {
+    CUtensorMap ta, tb;
+    int bn = 256;
+    bool a_mn = false, b_mn = false, k_grouped = false;
+    int epi = EPI_STORE_BF16;
+    int grid = 0;  // 0 = one CTA per SM
+};
+
+moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s);
+moe_status tmap_kmajor(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int box_rows);
+moe_status tmap_mnmajor(CUtensorMap* m, const void* base, int64_t krows, int64_t mn);
+
+}  // namespace moe
+
+extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b, void* d_d,
+                                       int32_t groups, const int32_t* d_group_rows,
+                                       int64_t total_rows, int64_t M, int64_t N, int64_t K,
+                                       int32_t a_mn_major, int32_t b_mn_major,
+                                       int32_t k_grouped, int32_t out_f32, int32_t bn,
+                                       moe_stream_t stream);

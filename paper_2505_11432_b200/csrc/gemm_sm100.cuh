@@ -1,0 +1,401 @@
+// gemm_sm100.cuh — persistent, warp-specialised tcgen05 grouped GEMM for the
+// expert FFN (the reference's `fc1` / `fc2` grouped_gemm nodes,
+// graph.cpp:260-261,289,296, and their backward at 2x cost, graph.cpp:345).
+//
+//   D_g[M, N] = A_g[M, K] . B_g[N, K]^T    (bf16 in, fp32 accumulate in TMEM)
+//
+// Two grouping modes:
+//   M-grouped (forward fc1/fc2 and both dgrads): groups are expert row
+//     segments of a permuted activation matrix, each padded to a multiple of
+//     128 rows; B_g is expert g's weight.
+//   K-grouped (wgrads): D_g = sum over expert g's rows; the rows are the
+//     contraction dimension.
+// Operands are K-major or MN-major (template flags) so dgrad/wgrad read the
+// forward layouts directly (no transposes in HBM).
+//
+// Roles (192 threads, 1 CTA per SM, persistent over a static tile stride):
+//   warp 0 lane 0 : TMA producer (4-stage smem ring, 128B swizzle)
+//   warp 1        : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN)
+//   warps 2..5    : epilogue (tcgen05.ld -> fused op -> global), TMEM
+//                   double-buffered so tile i's epilogue overlaps tile i+1's
+//                   MMA.
+#pragma once
+
+#include "common.cuh"
+
+namespace moe {
+
+enum EpiKind : int {
+    EPI_STORE_BF16 = 0,   // D -> bf16 rows (optionally x row gate)
+    EPI_STORE_F32 = 1,    // D -> fp32 rows
+    EPI_SWIGLU = 2,       // fc1: store fc1_out (bf16) and fc2_in = a*silu(b)*gate
+    EPI_SCATTER = 3,      // fc2 / fc1-dgrad: rows -> (rank, slot row) staging
+    EPI_SWIGLU_BWD = 4,   // fc2-dgrad: SwiGLU+gate backward, remat fc2_in, dgate partials
+};
+
+struct GemmArgs {
+    int G;                      // number of groups (local experts)
+    const int* group_rows;      // [G] padded rows per group (multiple of 128)
+    int N;                      // output columns
+    int K;                      // M-grouped: contraction length; K-grouped: output rows M
+    int b_group_stride;         // B coordinate offset per group (rows or K-rows)
+    // epilogue
+    void* out;                  // base of D (or fc1_out for SWIGLU, dfc1 for SWIGLU_BWD)
+    int64_t ldo;                // leading dimension of out (elements)
+    void* out2;                 // SWIGLU: fc2_in; SWIGLU_BWD: remat fc2_in
+    int64_t ldo2;
+    const float* row_gate;      // [padded rows] gate per permuted row (0 for pad rows)
+    const uint16_t* aux;        // SWIGLU_BWD: fc1_out (bf16 bits)
+    int64_t ld_aux;
+    float* row_part;            // SWIGLU_BWD: dgate partials [padded rows][n_tiles]
+    const int* row_dst;         // SCATTER: (rank << 27) | slot_row, -1 = skip
+    void* const* rank_base;     // SCATTER: per destination rank base pointer
+    int gate_rows;              // 1: multiply rows by row_gate in STORE/SCATTER epilogue
+};
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int BM = 128;
+    static constexpr int BK = 64;
+    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int MAX_GROUPS = 256;
+    static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES +
+                                      (2 * STAGES + 4) * 8 + 16;
+    static constexpr int THREADS = 192;
+};
+
+// Tile-sequence helper shared by all roles.
+struct TileInfo {
+    int g, m, n, kblocks, row0;
+};
+
+template <int BN, bool K_GROUPED>
+__device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const int* row_off,
+                                                const GemmArgs& a, int G, int n_tiles) {
+    // binary search the group whose tile range contains t
+    int lo = 0, hi = G - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    TileInfo ti;
+    ti.g = lo;
+    int li = t - prefix[lo];
+    if (!K_GROUPED) {
+        const int mt = a.group_rows[lo] >> 7;
+        ti.n = li / mt;
+        ti.m = li - ti.n * mt;
+        ti.kblocks = (a.K + 63) / 64;
+        ti.row0 = row_off[lo] + ti.m * 128;
+    } else {
+        const int mt = a.K >> 7;  // output rows / 128
+        ti.m = li % mt;
+        ti.n = li / mt;
+        ti.kblocks = a.group_rows[lo] >> 6;
+        ti.row0 = row_off[lo];   // contraction row offset
+    }
+    (void)n_tiles;
+    return ti;
+}
+
+template <int BN, bool A_MN, bool B_MN, bool K_GROUPED, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+    using Cfg = GemmCfg<BN>;
+    constexpr int BM = Cfg::BM, STAGES = Cfg::STAGES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty_bar = full_bar + STAGES;
+    uint64_t* tfull_bar = empty_bar + STAGES;
+    uint64_t* tempty_bar = tfull_bar + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    __shared__ int prefix[Cfg::MAX_GROUPS + 1];    // tile prefix per group
+    __shared__ int s_rowoff[Cfg::MAX_GROUPS + 1];  // padded row offset per group
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int G = args.G;
+    const int n_tiles = (args.N + BN - 1) / BN;
+
+    // --- setup: tile prefix + group row offsets (G <= MAX_GROUPS) -----------
+    if (threadIdx.x == 0) {
+        int acc = 0, racc = 0;
+        for (int g = 0; g < G; ++g) {
+            prefix[g] = acc;
+            s_rowoff[g] = racc;
+            const int rows = args.group_rows[g];
+            racc += rows;
+            if (!K_GROUPED) acc += (rows >> 7) * n_tiles;
+            else acc += (args.K >> 7) * n_tiles;
+        }
+        prefix[G] = acc;
+        s_rowoff[G] = racc;
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull_bar[a], 1);
+            mbar_init(&tempty_bar[a], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int total_tiles = prefix[G];
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                const TileInfo ti = decode_tile<BN, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+                for (int kb = 0; kb < ti.kblocks; ++kb) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+                    uint8_t* sb = sa + Cfg::A_BYTES;
+                    mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+                    if (!K_GROUPED) {
+                        // A: permuted activations [rows, K] (K-major) or [K..] n/a
+                        if (!A_MN) {
+                            tma_load_2d(sa, &tmA, &full_bar[stage], kb * 64, ti.row0);
+                        }
+                        if (!B_MN) {
+                            tma_load_2d(sb, &tmB, &full_bar[stage], kb * 64,
+                                        ti.g * args.b_group_stride + ti.n * BN);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage],
+                                            ti.n * BN + j * 64,
+                                            ti.g * args.b_group_stride + kb * 64);
+                        }
+                    } else {
+                        // wgrad: A = [rows, M] MN-major, B = [rows, N] MN-major
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j)
+                            tma_load_2d(sa + j * 8192, &tmA, &full_bar[stage], ti.m * BM + j * 64,
+                                        ti.row0 + kb * 64);
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j)
+                            tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], ti.n * BN + j * 64,
+                                        ti.row0 + kb * 64);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc(BM, BN, 1, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                const TileInfo ti = decode_tile<BN, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+                if (ti.kblocks == 0) continue;
+                mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < ti.kblocks; ++kb) {
+                    mbar_wait(&full_bar[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                    const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t ad = A_MN ? make_sdesc(sa + kk * 2048, 8192, 1024)
+                                                 : make_sdesc(sa + kk * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? make_sdesc(sb + kk * 2048, 8192, 1024)
+                                                 : make_sdesc(sb + kk * 32, 16, 1024);
+                        umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    umma_commit(&empty_bar[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(&tfull_bar[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ===================== epilogue (warps 2..5) =====================
+        const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+        const int r_in_tile = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const TileInfo ti = decode_tile<BN, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+            const int n0 = ti.n * BN;
+            // output row (global) for this thread
+            const int64_t orow = K_GROUPED ? (int64_t)ti.g * args.K + ti.m * BM + r_in_tile
+                                           : (int64_t)ti.row0 + r_in_tile;
+            if (ti.kblocks == 0) {
+                // empty contraction (expert received no rows): D = 0
+                if (EPI == EPI_STORE_BF16) {
+                    uint16_t* o = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
+                    for (int c = 0; c < BN; c += 8)
+                        if (n0 + c < args.N) *reinterpret_cast<uint4*>(o + c) = make_uint4(0, 0, 0, 0);
+                } else if (EPI == EPI_STORE_F32) {
+                    float* o = reinterpret_cast<float*>(args.out) + orow * args.ldo + n0;
+                    for (int c = 0; c < BN; c += 4)
+                        if (n0 + c < args.N) *reinterpret_cast<float4*>(o + c) = make_float4(0, 0, 0, 0);
+                }
+                continue;
+            }
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+
+            if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32 || EPI == EPI_SCATTER) {
+                float gscale = 1.0f;
+                if (args.gate_rows) gscale = args.row_gate[orow];
+                uint16_t* obf = nullptr;
+                float* of32 = nullptr;
+                bool valid = true;
+                if (EPI == EPI_SCATTER) {
+                    const int dst = args.row_dst[orow];
+                    valid = dst >= 0;
+                    if (valid)
+                        obf = reinterpret_cast<uint16_t*>(args.rank_base[dst >> 27]) +
+                              (int64_t)(dst & ((1 << 27) - 1)) * args.ldo + n0;
+                } else if (EPI == EPI_STORE_BF16) {
+                    obf = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
+                } else {
+                    of32 = reinterpret_cast<float*>(args.out) + orow * args.ldo + n0;
+                }
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tbase + c0, r);
+                    tmem_ld_wait();
+                    if (!valid || n0 + c0 >= args.N) continue;
+                    if (EPI == EPI_STORE_F32) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            float4 v = make_float4(__uint_as_float(r[i]) * gscale,
+                                                   __uint_as_float(r[i + 1]) * gscale,
+                                                   __uint_as_float(r[i + 2]) * gscale,
+                                                   __uint_as_float(r[i + 3]) * gscale);
+                            *reinterpret_cast<float4*>(of32 + c0 + i) = v;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 8) {
+                            uint4 v;
+                            v.x = pack_bf16x2(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale);
+                            v.y = pack_bf16x2(__uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
+                            v.z = pack_bf16x2(__uint_as_float(r[i + 4]) * gscale, __uint_as_float(r[i + 5]) * gscale);
+                            v.w = pack_bf16x2(__uint_as_float(r[i + 6]) * gscale, __uint_as_float(r[i + 7]) * gscale);
+                            *reinterpret_cast<uint4*>(obf + c0 + i) = v;
+                        }
+                    }
+                }
+            } else if constexpr (EPI == EPI_SWIGLU) {
+                // accumulator cols [0,BN/2) = a block, [BN/2,BN) = b block
+                // (W1 rows interleaved per BN/2 block at weight-pack time)
+                const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
+                uint16_t* o1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
+                uint16_t* o2 = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2 + ti.n * (BN / 2);
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN / 2; c0 += 32) {
+                    uint32_t ra[32], rb[32];
+                    tmem_ld32(tbase + c0, ra);
+                    tmem_ld32(tbase + BN / 2 + c0, rb);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8) {
+                        uint32_t pa[4], pb[4], ph[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            pa[q] = pack_bf16x2(__uint_as_float(ra[i + 2 * q]), __uint_as_float(ra[i + 2 * q + 1]));
+                            pb[q] = pack_bf16x2(__uint_as_float(rb[i + 2 * q]), __uint_as_float(rb[i + 2 * q + 1]));
+                            // SwiGLU on the bf16-rounded fc1_out so backward remat is exact
+                            const float2 a2 = unpack_bf16x2(pa[q]);
+                            const float2 b2 = unpack_bf16x2(pb[q]);
+                            ph[q] = pack_bf16x2(a2.x * silu_f(b2.x) * g, a2.y * silu_f(b2.y) * g);
+                        }
+                        *reinterpret_cast<uint4*>(o1 + c0 + i) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+                        *reinterpret_cast<uint4*>(o1 + BN / 2 + c0 + i) = make_uint4(pb[0], pb[1], pb[2], pb[3]);
+                        *reinterpret_cast<uint4*>(o2 + c0 + i) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+                    }
+                }
+            } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+                // D = d fc2_in for f-columns [n0, n0+BN). fc1_out / dfc1 are in the
+                // interleaved [a-block(128) | b-block(128)] layout.
+                const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
+                const uint16_t* f1 = args.aux + orow * args.ld_aux;
+                uint16_t* d1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo;
+                uint16_t* rf = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2;
+                float dg = 0.0f;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tbase + c0, r);
+                    const int j = n0 + c0;           // f column
+                    const int ia = (j >> 7) * 256 + (j & 127);
+                    uint4 av[4], bv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        av[q] = *reinterpret_cast<const uint4*>(f1 + ia + q * 8);
+                        bv[q] = *reinterpret_cast<const uint4*>(f1 + ia + 128 + q * 8);
+                    }
+                    tmem_ld_wait();
+                    uint32_t da[16], db[16], hf[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const uint32_t aw = (&av[q >> 2].x)[q & 3];
+                        const uint32_t bw = (&bv[q >> 2].x)[q & 3];
+                        const float2 a2 = unpack_bf16x2(aw);
+                        const float2 b2 = unpack_bf16x2(bw);
+                        const float d0 = __uint_as_float(r[2 * q]), d1v = __uint_as_float(r[2 * q + 1]);
+                        const float s0 = 1.0f / (1.0f + __expf(-b2.x)), s1 = 1.0f / (1.0f + __expf(-b2.y));
+                        const float si0 = b2.x * s0, si1 = b2.y * s1;
+                        dg += d0 * a2.x * si0 + d1v * a2.y * si1;
+                        da[q] = pack_bf16x2(d0 * g * si0, d1v * g * si1);
+                        db[q] = pack_bf16x2(d0 * g * a2.x * s0 * (1.0f + b2.x * (1.0f - s0)),
+                                            d1v * g * a2.y * s1 * (1.0f + b2.y * (1.0f - s1)));
+                        hf[q] = pack_bf16x2(a2.x * si0 * g, a2.y * si1 * g);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        *reinterpret_cast<uint4*>(d1 + ia + q * 8) = make_uint4(da[4 * q], da[4 * q + 1], da[4 * q + 2], da[4 * q + 3]);
+                        *reinterpret_cast<uint4*>(d1 + ia + 128 + q * 8) = make_uint4(db[4 * q], db[4 * q + 1], db[4 * q + 2], db[4 * q + 3]);
+                        *reinterpret_cast<uint4*>(rf + j + q * 8) = make_uint4(hf[4 * q], hf[4 * q + 1], hf[4 * q + 2], hf[4 * q + 3]);
+                    }
+                }
+                if (args.row_part) args.row_part[orow * n_tiles + ti.n] = dg;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+
+    __syncwarp();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    }
+}
+
+}  // namespace moe
