@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark: MoE layer forward+backward tokens/s on B200 (BASELINE.json
+metric), Mixtral-8x7B-shape layer (configs[1]): hidden 4096, ffn 14336,
+8 experts top-2, bf16, 4096 tokens per rank, EP = number of GPUs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0. Under torchrun (N > 1) every rank runs one process
+per GPU; the layer's dispatch/combine go over NVLink inside the kernels.
+
+`--impl reference`: the reference's CPU path on this host (rank 0 only):
+its own routing code (oracle/_ref, compiled from the reference sources) plus
+the fp32 oracle port of the dense math (the reference has none), on a bounded
+token sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "mixtral": dict(workload="mixtral-8x7b-moe-layer-fwd+bwd", hidden=4096, ffn_hidden=14336,
+                    num_experts=8, top_k=2, tokens_per_rank=4096),
+    "deepseek": dict(workload="deepseek-v3-moe-layer-fwd+bwd", hidden=7168, ffn_hidden=2048,
+                     num_experts=256, top_k=8, tokens_per_rank=4096),
+    "small": dict(workload="small-moe-layer-fwd+bwd", hidden=1024, ffn_hidden=2816,
+                  num_experts=8, top_k=2, tokens_per_rank=4096),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d["bf16_tflops_sustained"],
+                    src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([v.strip() for v in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > i + 2 and s[i + 2] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+_CPU_STATE = {}
+
+
+def cpu_reference_step(cfg, sample_tokens, seed=0, with_dense=True):
+    """One step of the reference CPU path on a bounded sample: the
+    reference's own routing maps (oracle/_ref) + the fp32 oracle's dense
+    fwd+bwd for `sample_tokens` tokens. Returns (seconds, kind, threads)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as P
+    h, f, E, k = cfg["hidden"], cfg["ffn_hidden"], cfg["num_experts"], cfg["top_k"]
+    S = sample_tokens
+    key = (h, f, E, k, S)
+    if key not in _CPU_STATE:  # weights generated once (not timed)
+        rng = np.random.default_rng(0)
+        w1 = rng.standard_normal((E, 2 * f, h), dtype=np.float32)
+        w1 *= np.float32(1.0 / np.sqrt(h))
+        w2 = rng.standard_normal((E, h, f), dtype=np.float32)
+        w2 *= np.float32(1.0 / np.sqrt(f))
+        wr = (rng.standard_normal((E, h), dtype=np.float32) / np.float32(np.sqrt(h)))
+        _CPU_STATE.clear()
+        _CPU_STATE[key] = (w1, w2, wr)
+    w1, w2, wr = _CPU_STATE[key]
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal((S, h), dtype=np.float32) * np.float32(0.5))
+    dy = (rng.standard_normal((S, h), dtype=np.float32) * np.float32(0.1))
+    kind = "reference" if P.ref_available() else "port"
+    t0 = time.perf_counter()
+    logits, ex, gates = P.orc_router_topk(x, wr, k)
+    src = np.zeros(S, np.int32)
+    dr = np.zeros(S, np.uint8)
+    if kind == "reference":
+        m = P.ref_build_scatter_map(ex, src, dr, E, 1, 0)
+        P.ref_sort_tokens_for_tiles(ex, src, dr, E, 1, 0, 128)
+    else:
+        m = P.orc_build_scatter_map(ex, src, dr, E, 1, 0)
+        P.orc_sort_tokens_for_tiles(m["out_expert"], m["out_source_rank"], 128)
+    if with_dense:
+        P.orc_moe_forward(x, ex, gates, dr, w1, w2)
+        P.orc_moe_backward(x, dy, ex, gates, logits, dr, w1, w2, wr)
+    dt = time.perf_counter() - t0
+    return dt, kind, os.cpu_count()
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    S = args.cpu_sample
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, kind, cores = cpu_reference_step(cfg, S, seed=i)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * float(np.mean(times))
+    val = S / (ms / 1000.0)
+    line = {
+        "impl": "reference", "metric": "moe_layer_fwd_bwd_tokens_per_s", "value": val,
+        "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "hidden": cfg["hidden"], "ffn_hidden": cfg["ffn_hidden"],
+                   "num_experts": cfg["num_experts"], "top_k": cfg["top_k"],
+                   "tokens_per_rank": cfg["tokens_per_rank"], "sample_tokens_per_step": S},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": kind,
+                         "sample": f"{S} tokens/step: reference routing maps (oracle/_ref) + fp32 "
+                                   f"oracle router+FFN fwd+bwd incl. weight grads, OpenMP {cores} threads"},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2505_11432_b200 import launch_count, launch_count_reset
+    from paper_2505_11432_b200.layer import MoELayer
+
+    h, f, E, k, Tr = cfg["hidden"], cfg["ffn_hidden"], cfg["num_experts"], cfg["top_k"], cfg["tokens_per_rank"]
+    n = world
+    el = E // n
+    g = torch.Generator(device="cuda").manual_seed(42)
+    w1 = (torch.randn(el, 2 * f, h, device="cuda", generator=g) / h ** 0.5).bfloat16()
+    w2 = (torch.randn(el, h, f, device="cuda", generator=g) / f ** 0.5).bfloat16()
+    wr = (torch.randn(E, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7)) / h ** 0.5).bfloat16()
+    L = MoELayer(Tr, h, f, E, k, ep_size=n, rank=rank, capacity_factor=0.0,
+                 gate_order="before_fc2_in", route_mode="learned")
+    L.set_weights(w1, w2, wr)
+    del w1, w2
+    if n > 1:
+        L.connect()
+    gx = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = (torch.randn(Tr, h, device="cuda", generator=gx) * 0.5).bfloat16()
+    dy = (torch.randn(Tr, h, device="cuda", generator=gx) * 0.1).bfloat16()
+    L.input_buffer.copy_(x)
+    dx = torch.empty(Tr, h, dtype=torch.bfloat16, device="cuda")
+    dw1 = torch.empty(el, 2 * f, h, dtype=torch.bfloat16, device="cuda")
+    dw2 = torch.empty(el, h, f, dtype=torch.bfloat16, device="cuda")
+    dwr = torch.empty(E, h, dtype=torch.float32, device="cuda")
+    y = torch.empty(Tr, h, dtype=torch.bfloat16, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        L.forward(None, y)
+        L.backward(dy, dx, dw1, dw2, dwr)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    sync_all()
+    if L.error_flag():
+        raise RuntimeError("cross-GPU flag wait timed out during warm-up")
+
+    # ---- device-timed region (inputs resident in HBM) ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    launch_count_reset()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sync_all()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    sync_all()
+    launches = launch_count()
+    clk = clocks.stop()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms_local], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = n * Tr / (ms / 1000.0)
+
+    # ---- per-phase device times (one instrumented step, same stream) ----
+    L.enable_timing(True)
+    phases = {}
+    reps = 3
+    for _ in range(reps):
+        L.forward(None, y)
+        L.backward(dy, dx, dw1, dw2, dwr)   # back to back: no idle gap between phases
+        for kk, v in L.phase_times().items():
+            phases[kk] = phases.get(kk, 0.0) + v / reps
+    L.enable_timing(False)
+    sync_all()
+
+    # ---- end-to-end through the public API with host buffers ----
+    x_h = x.cpu().pin_memory()
+    dy_h = dy.cpu().pin_memory()
+    dx_h = torch.empty(Tr, h, dtype=torch.bfloat16).pin_memory()
+    x_d = torch.empty_like(x)
+    dy_d = torch.empty_like(dy)
+
+    def e2e_step():
+        x_d.copy_(x_h, non_blocking=True)
+        dy_d.copy_(dy_h, non_blocking=True)
+        L.forward(x_d, y)
+        L.backward(dy_d, dx, dw1, dw2, dwr)
+        dx_h.copy_(dx, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    sync_all()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    sync_all()
+    te = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+
+    if rank == 0:
+        peaks = load_peaks()
+        rows = Tr * k * n  # expert rows processed per rank (uniform expectation)
+        rows_local = Tr * k  # per rank in expectation (weak scaling)
+        fc1_flops = 2.0 * rows_local * h * 2 * f
+        fc1_ms = phases.get("fc1", float("nan"))
+        achieved = fc1_flops / (fc1_ms / 1000.0) / 1e12
+        total_flops = 3.0 * rows_local * 6.0 * h * f  # fwd+bwd expert FFN
+        line = {
+            "metric": "moe_layer_fwd_bwd_tokens_per_s", "value": value, "unit": "tokens/s",
+            "n_gpus": n, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, N(0,0.25) tokens; learned router)",
+            "config": {"workload": cfg["workload"], "hidden": h, "ffn_hidden": f, "num_experts": E,
+                       "top_k": k, "tokens_per_rank": Tr, "global_tokens": Tr * n,
+                       "parallelism": f"ep{n}", "l2": "inputs larger than L2 (weights 2.8 GB/layer)"},
+            "roofline": {"bound": "tensor", "kernel": "fc1 grouped GEMM (tcgen05) + fused SwiGLU",
+                         "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
+                         "frac": achieved / peaks["bf16_sus"], "traffic": None,
+                         "peak_kind": f"bf16 sustained ({peaks['src']})",
+                         "step_tflops": total_flops / (ms / 1000.0) / 1e12,
+                         "step_frac": total_flops / (ms / 1000.0) / 1e12 / peaks["bf16_sus"]},
+            "phases_ms": {kk: round(v, 4) for kk, v in phases.items()},
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "e2e": {"value": n * Tr / (e2e_ms / 1000.0), "unit": "tokens/s",
+                    "h2d_bytes_per_step": 2 * Tr * h * 2, "d2h_bytes_per_step": Tr * h * 2,
+                    "ms_per_step": e2e_ms},
+        }
+        if n == 1 and not args.no_cpu_baseline:
+            try:
+                dt, kind, cores = cpu_reference_step(cfg, args.cpu_sample)
+                line["cpu_baseline"] = {
+                    "value": args.cpu_sample / dt, "unit": "tokens/s", "cores": cores, "kind": kind,
+                    "sample": f"{args.cpu_sample} tokens: reference routing maps + fp32 oracle "
+                              f"router+FFN fwd+bwd incl. weight grads ({cores} OpenMP threads)"}
+            except Exception as e:  # noqa: BLE001
+                line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-sample", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

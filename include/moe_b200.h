@@ -216,6 +216,15 @@ moe_status moe_layer_enable_timing(moe_layer* L, int enable);
 moe_status moe_layer_phase_times(moe_layer* L, float* h_ms, int max_phases, int* n_phases,
                                  const char** names);
 
+/* Non-zero if a cross-GPU flag wait of this layer timed out (synchronous). */
+int moe_layer_error_flag(moe_layer* L);
+
+/* Generic grouped GEMM (reference OpKind::grouped_gemm): see gemm.h. */
+moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b, void* d_d, int32_t groups,
+                            const int32_t* d_group_rows, int64_t total_rows, int64_t M, int64_t N,
+                            int64_t K, int32_t a_mn_major, int32_t b_mn_major, int32_t k_grouped,
+                            int32_t out_f32, int32_t bn, moe_stream_t stream);
+
 /* ===================================================================== */
 /* Multi-GPU fabric (NVLink P2P over NVSwitch; one process per GPU)       */
 /* ===================================================================== */

@@ -1,6 +1,8 @@
 // gemm.cu — host launchers for the tcgen05 grouped GEMM (gemm_sm100.cuh)
 // and the C-ABI `moe_grouped_gemm` operator (reference OpKind::grouped_gemm,
 // simsched.hpp:32-44).
+#include <cstdlib>
+
 #include "gemm.h"
 
 namespace moe {
@@ -70,6 +72,8 @@ extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b,
                                        int32_t a_mn_major, int32_t b_mn_major,
                                        int32_t k_grouped, int32_t out_f32, int32_t bn,
                                        moe_stream_t stream) {
+    const char* env = getenv("MOE_B_BOX_ROWS");
+    const int b_box = env ? atoi(env) : 0;
     MOE_CHECK_ARG(d_a && d_b && d_d && d_group_rows, "null pointer");
     MOE_CHECK_ARG(bn == 128 || bn == 256, "bn must be 128 or 256");
     MOE_CHECK_ARG(N % 64 == 0 && K % 64 == 0 && M % 128 == 0 || !k_grouped, "K-grouped: M%128, N%64, K%64");
@@ -93,7 +97,8 @@ extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b,
         MOE_TRY(tmap_kmajor(&p.ta, d_a, total_rows, K, 128));
         if (!b_mn_major) {
             a.b_group_stride = (int)N;
-            MOE_TRY(tmap_kmajor(&p.tb, d_b, (int64_t)groups * N, K, bn));
+            a.b_box_rows = b_box > 0 ? b_box : bn;
+            MOE_TRY(tmap_kmajor(&p.tb, d_b, (int64_t)groups * N, K, a.b_box_rows));
         } else {
             a.b_group_stride = (int)K;
             MOE_TRY(tmap_mnmajor(&p.tb, d_b, (int64_t)groups * K, N));

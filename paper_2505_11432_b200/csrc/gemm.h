@@ -20,9 +20,3 @@ moe_status tmap_mnmajor(CUtensorMap* m, const void* base, int64_t krows, int64_t
 
 }  // namespace moe
 
-extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b, void* d_d,
-                                       int32_t groups, const int32_t* d_group_rows,
-                                       int64_t total_rows, int64_t M, int64_t N, int64_t K,
-                                       int32_t a_mn_major, int32_t b_mn_major,
-                                       int32_t k_grouped, int32_t out_f32, int32_t bn,
-                                       moe_stream_t stream);

@@ -51,6 +51,9 @@ struct GemmArgs {
     const int* row_dst;         // SCATTER: (rank << 27) | slot_row, -1 = skip
     void* const* rank_base;     // SCATTER: per destination rank base pointer
     int gate_rows;              // 1: multiply rows by row_gate in STORE/SCATTER epilogue
+    int b_box_rows;             // K-major B: rows per TMA box (BN or 64)
+    int interleave_rows;        // K-grouped STORE: map packed a/b-interleaved rows back to
+                                // the reference [a | b] row order (dW1)
 };
 
 template <int BN>
@@ -177,8 +180,10 @@ __global__ void __launch_bounds__(192, 1)
                             tma_load_2d(sa, &tmA, &full_bar[stage], kb * 64, ti.row0);
                         }
                         if (!B_MN) {
-                            tma_load_2d(sb, &tmB, &full_bar[stage], kb * 64,
-                                        ti.g * args.b_group_stride + ti.n * BN);
+                            const int bbr = args.b_box_rows > 0 ? args.b_box_rows : BN;
+                            for (int j = 0; j < BN; j += bbr)
+                                tma_load_2d(sb + j * 128, &tmB, &full_bar[stage], kb * 64,
+                                            ti.g * args.b_group_stride + ti.n * BN + j);
                         } else {
 #pragma unroll
                             for (int j = 0; j < BN / 64; ++j)
@@ -245,8 +250,17 @@ __global__ void __launch_bounds__(192, 1)
             const TileInfo ti = decode_tile<BN, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
             const int n0 = ti.n * BN;
             // output row (global) for this thread
-            const int64_t orow = K_GROUPED ? (int64_t)ti.g * args.K + ti.m * BM + r_in_tile
-                                           : (int64_t)ti.row0 + r_in_tile;
+            int64_t orow;
+            if (K_GROUPED) {
+                int mi = ti.m * BM + r_in_tile;
+                if (args.interleave_rows) {
+                    const int blk = mi >> 8, w = mi & 255;
+                    mi = w < 128 ? blk * 128 + w : (args.K >> 1) + blk * 128 + (w - 128);
+                }
+                orow = (int64_t)ti.g * args.K + mi;
+            } else {
+                orow = (int64_t)ti.row0 + r_in_tile;
+            }
             if (ti.kblocks == 0) {
                 // empty contraction (expert received no rows): D = 0
                 if (EPI == EPI_STORE_BF16) {

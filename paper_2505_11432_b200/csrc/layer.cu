@@ -1,0 +1,627 @@
+// layer.cu — the MoE layer handle: router -> dispatch (AG + local scatter)
+// -> fc1 GroupedGEMM + SwiGLU (+ gate) -> fc2 GroupedGEMM + gather to the
+// source rank -> combine, and the mirrored backward with the paper's
+// selective rematerialisation of fc2_in from the retained fc1_out
+// (graph.cpp:254-311 forward, :333-401 backward).
+//
+// Multi-GPU (ep_size = n > 1): one process per GPU. Every rank owns one
+// symmetric arena (identical offsets on every rank) exported with CUDA IPC;
+// peers' arenas are mapped over NVLink. Dispatch pulls token rows straight
+// from the owning rank's input buffer into permuted order; the fc2 epilogue
+// stores each output row into the owning rank's combine staging; device
+// flag barriers (st.release.sys / ld.acquire.sys) separate the phases.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gemm.h"
+#include "layer_kernels.cuh"
+#include "runtime.h"
+
+namespace moe {
+
+namespace {
+size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+}  // namespace
+
+enum Phase {
+    PH_ROUTE, PH_PERMUTE, PH_DISPATCH, PH_FC1, PH_FC2, PH_COMBINE, PH_FWD_END,
+    PH_DISPATCH_DY, PH_FC2_DGRAD, PH_FC2_WGRAD, PH_FC1_DGRAD, PH_FC1_WGRAD, PH_DGATE,
+    PH_COMBINE_DX, PH_ROUTER_WGRAD, PH_END, PH_COUNT
+};
+static const char* kPhaseNames[PH_COUNT] = {
+    "route", "permute", "dispatch", "fc1", "fc2", "combine", "fwd_end", "dispatch_dy", "fc2_dgrad",
+    "fc2_wgrad", "fc1_dgrad", "fc1_wgrad", "dgate", "combine_dx", "router_wgrad", "end"};
+
+}  // namespace moe
+
+struct moe_layer {
+    moe_layer_config cfg{};
+    int64_t Tr = 0, T = 0, h = 0, f = 0, E = 0, k = 0, n = 1, rank = 0, el = 0, first = 0, Mp = 0;
+    int dev = 0;
+    // symmetric arena (IPC-exported)
+    uint8_t* arena = nullptr;
+    size_t arena_bytes = 0;
+    size_t off_x = 0, off_dy = 0, off_stage = 0, off_dstage = 0, off_ex = 0, off_gt = 0,
+           off_dgate = 0, off_flags = 0;
+    std::vector<uint8_t*> peer_arena;  // [n], self included
+    // local buffers
+    uint16_t *w1p = nullptr, *w2 = nullptr, *wr = nullptr;
+    int32_t* ex_loc = nullptr;
+    float *gt_loc = nullptr, *logits = nullptr;
+    int32_t* src = nullptr;
+    uint8_t* dropped = nullptr;
+    void* perm_ws = nullptr;
+    int32_t *row_map_in = nullptr, *out_expert = nullptr, *out_src = nullptr, *counts = nullptr,
+            *expert_off = nullptr, *rows = nullptr, *gpad_rows = nullptr, *gpad_off = nullptr,
+            *pad_tok = nullptr, *row_dst = nullptr;
+    float* row_gate = nullptr;
+    uint16_t *x_perm = nullptr, *fc1_out = nullptr, *fc2_in = nullptr, *dy_perm = nullptr,
+             *dfc1 = nullptr;
+    float *dgate_part = nullptr, *dlogits = nullptr, *rw_part = nullptr;
+    // device pointer tables [n]
+    const uint16_t** t_x = nullptr;
+    const uint16_t** t_dy = nullptr;
+    void** t_stage = nullptr;
+    void** t_dstage = nullptr;
+    int32_t** t_ex = nullptr;
+    float** t_gt = nullptr;
+    float** t_dgate = nullptr;
+    uint32_t** t_flags = nullptr;
+    int* err = nullptr;
+    uint32_t epoch = 0;
+    bool router_attr = false;
+    bool weights_set = false, routing_set = false, fwd_done = false, ipc_ready = false;
+    // GEMM plans (tensor maps fixed at create / set_weights)
+    moe::GemmPlan p_fc1, p_fc2, p_fc2_dgrad, p_fc2_wgrad, p_fc1_dgrad, p_fc1_wgrad;
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[moe::PH_COUNT] = {};
+    bool ev_used[moe::PH_COUNT] = {};
+
+    uint16_t* x_sym() { return reinterpret_cast<uint16_t*>(arena + off_x); }
+    uint16_t* dy_sym() { return reinterpret_cast<uint16_t*>(arena + off_dy); }
+    uint16_t* stage_sym() { return reinterpret_cast<uint16_t*>(arena + off_stage); }
+    uint16_t* dstage_sym() { return reinterpret_cast<uint16_t*>(arena + off_dstage); }
+    int32_t* ex_all() { return reinterpret_cast<int32_t*>(arena + off_ex); }
+    float* gt_all() { return reinterpret_cast<float*>(arena + off_gt); }
+    float* dgate_sym() { return reinterpret_cast<float*>(arena + off_dgate); }
+    void mark(int ph, cudaStream_t s) {
+        if (timing) {
+            cudaEventRecord(ev[ph], s);
+            ev_used[ph] = true;
+        }
+    }
+};
+
+using namespace moe;
+
+namespace {
+
+template <class T>
+moe_status dalloc(T** p, size_t count) {
+    MOE_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+    return MOE_OK;
+}
+
+moe_status fill_tables(moe_layer* L) {
+    const int n = (int)L->n;
+    std::vector<const uint16_t*> tx(n), tdy(n);
+    std::vector<void*> ts(n), tds(n);
+    std::vector<int32_t*> te(n);
+    std::vector<float*> tg(n), tdg(n);
+    std::vector<uint32_t*> tf(n);
+    for (int p = 0; p < n; ++p) {
+        uint8_t* a = L->peer_arena[p];
+        tx[p] = reinterpret_cast<const uint16_t*>(a + L->off_x);
+        tdy[p] = reinterpret_cast<const uint16_t*>(a + L->off_dy);
+        ts[p] = a + L->off_stage;
+        tds[p] = a + L->off_dstage;
+        te[p] = reinterpret_cast<int32_t*>(a + L->off_ex);
+        tg[p] = reinterpret_cast<float*>(a + L->off_gt);
+        tdg[p] = reinterpret_cast<float*>(a + L->off_dgate);
+        tf[p] = reinterpret_cast<uint32_t*>(a + L->off_flags);
+    }
+    MOE_CUDA_TRY(cudaMemcpy(L->t_x, tx.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->t_dy, tdy.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->t_stage, ts.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->t_dstage, tds.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->t_ex, te.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->t_gt, tg.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->t_dgate, tdg.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->t_flags, tf.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    return MOE_OK;
+}
+
+moe_status build_plans(moe_layer* L) {
+    const int64_t Mp = L->Mp, h = L->h, f = L->f, el = L->el;
+    // forward fc1: A = x_perm [Mp, h], B = w1p [el*2f, h] (K-major)
+    L->p_fc1 = GemmPlan{};
+    L->p_fc1.epi = EPI_SWIGLU;
+    MOE_TRY(tmap_kmajor(&L->p_fc1.ta, L->x_perm, Mp, h, 128));
+    MOE_TRY(tmap_kmajor(&L->p_fc1.tb, L->w1p, el * 2 * f, h, 256));
+    // forward fc2: A = fc2_in [Mp, f], B = w2 [el*h, f] (K-major)
+    L->p_fc2 = GemmPlan{};
+    L->p_fc2.epi = EPI_SCATTER;
+    MOE_TRY(tmap_kmajor(&L->p_fc2.ta, L->fc2_in, Mp, f, 128));
+    MOE_TRY(tmap_kmajor(&L->p_fc2.tb, L->w2, el * h, f, 256));
+    // fc2 dgrad: A = dy_perm [Mp, h], B(n=f, k=h) = w2[e][k][n] (MN-major)
+    L->p_fc2_dgrad = GemmPlan{};
+    L->p_fc2_dgrad.epi = EPI_SWIGLU_BWD;
+    L->p_fc2_dgrad.b_mn = true;
+    MOE_TRY(tmap_kmajor(&L->p_fc2_dgrad.ta, L->dy_perm, Mp, h, 128));
+    MOE_TRY(tmap_mnmajor(&L->p_fc2_dgrad.tb, L->w2, el * h, f));
+    // fc2 wgrad: dW2[e] = dy_perm^T fc2_in (K-grouped, MN-major both)
+    L->p_fc2_wgrad = GemmPlan{};
+    L->p_fc2_wgrad.epi = EPI_STORE_BF16;
+    L->p_fc2_wgrad.a_mn = L->p_fc2_wgrad.b_mn = L->p_fc2_wgrad.k_grouped = true;
+    MOE_TRY(tmap_mnmajor(&L->p_fc2_wgrad.ta, L->dy_perm, Mp, h));
+    MOE_TRY(tmap_mnmajor(&L->p_fc2_wgrad.tb, L->fc2_in, Mp, f));
+    // fc1 dgrad: A = dfc1 [Mp, 2f], B(n=h, k=j) = w1p[e][j][n] (MN-major)
+    L->p_fc1_dgrad = GemmPlan{};
+    L->p_fc1_dgrad.epi = EPI_SCATTER;
+    L->p_fc1_dgrad.b_mn = true;
+    MOE_TRY(tmap_kmajor(&L->p_fc1_dgrad.ta, L->dfc1, Mp, 2 * f, 128));
+    MOE_TRY(tmap_mnmajor(&L->p_fc1_dgrad.tb, L->w1p, el * 2 * f, h));
+    // fc1 wgrad: dW1p[e] = dfc1^T x_perm (K-grouped)
+    L->p_fc1_wgrad = GemmPlan{};
+    L->p_fc1_wgrad.epi = EPI_STORE_BF16;
+    L->p_fc1_wgrad.a_mn = L->p_fc1_wgrad.b_mn = L->p_fc1_wgrad.k_grouped = true;
+    MOE_TRY(tmap_mnmajor(&L->p_fc1_wgrad.ta, L->dfc1, Mp, 2 * f));
+    MOE_TRY(tmap_mnmajor(&L->p_fc1_wgrad.tb, L->x_perm, Mp, h));
+    return MOE_OK;
+}
+
+moe_status barrier(moe_layer* L, int slot, cudaStream_t s) {
+    if (L->n == 1) return MOE_OK;
+    if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
+    flag_barrier_kernel<<<1, 64, 0, s>>>(L->t_flags, slot, (int)L->n, (int)L->rank, L->epoch,
+                                        20ull * 1000 * 1000 * 1000, L->err);
+    count_launch();
+    MOE_CUDA_TRY(cudaGetLastError());
+    return MOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
+    MOE_CHECK_ARG(cfg && out, "null argument");
+    const moe_layer_config c = *cfg;
+    MOE_CHECK_ARG(c.tokens_per_rank >= 1 && c.hidden >= 256 && c.ffn_hidden >= 256,
+                  "tokens_per_rank >= 1, hidden and ffn_hidden >= 256");
+    MOE_CHECK_ARG(c.hidden % 256 == 0, "hidden must be a multiple of 256");
+    MOE_CHECK_ARG(c.ffn_hidden % 256 == 0, "ffn_hidden must be a multiple of 256");
+    MOE_CHECK_ARG(c.num_experts >= 1 && c.top_k >= 1 && c.top_k <= 8 && c.top_k <= c.num_experts,
+                  "need 1 <= top_k <= min(8, num_experts)");
+    MOE_CHECK_ARG(c.ep_size >= 1 && c.ep_size <= 32 && c.num_experts % c.ep_size == 0,
+                  "num_experts must be divisible by ep_size (<= 32)");
+    MOE_CHECK_ARG(c.rank >= 0 && c.rank < c.ep_size, "rank out of range");
+    MOE_CHECK_ARG(c.num_experts / c.ep_size <= 256, "at most 256 local experts");
+    MOE_CHECK_ARG(c.comm_format == MOE_COMM_BF16, "FP8 communication is not enabled in this build of the layer");
+    auto* L = new moe_layer();
+    L->cfg = c;
+    L->Tr = c.tokens_per_rank;
+    L->n = c.ep_size;
+    L->rank = c.rank;
+    L->T = L->Tr * L->n;
+    L->h = c.hidden;
+    L->f = c.ffn_hidden;
+    L->E = c.num_experts;
+    L->k = c.top_k;
+    L->el = L->E / L->n;
+    L->first = L->rank * L->el;
+    L->Mp = L->T * L->k + L->el * 128;
+    MOE_CHECK_ARG(L->T * L->k < (1ll << 27), "T*k must be < 2^27");
+    cudaGetDevice(&L->dev);
+
+    // ---- symmetric arena ----
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
+    L->off_x = take(L->Tr * L->h * 2);
+    L->off_dy = take(L->Tr * L->h * 2);
+    L->off_stage = take(L->Tr * L->k * L->h * 2);
+    L->off_dstage = take(L->Tr * L->k * L->h * 2);
+    L->off_ex = take(L->T * L->k * 4);
+    L->off_gt = take(L->T * L->k * 4);
+    L->off_dgate = take(L->Tr * L->k * 4);
+    L->off_flags = take(16 * 64 * 4);
+    L->arena_bytes = off;
+    moe_status st = MOE_OK;
+#define TRY_ALLOC(expr) do { st = (expr); if (st != MOE_OK) { moe_layer_destroy(L); return st; } } while (0)
+    TRY_ALLOC(dalloc(&L->arena, L->arena_bytes));
+    cudaMemset(L->arena, 0, L->arena_bytes);
+    L->peer_arena.assign(L->n, nullptr);
+    L->peer_arena[L->rank] = L->arena;
+    const int64_t Mp = L->Mp, h = L->h, f = L->f, el = L->el;
+    TRY_ALLOC(dalloc(&L->w1p, el * 2 * f * h));
+    TRY_ALLOC(dalloc(&L->w2, el * h * f));
+    TRY_ALLOC(dalloc(&L->wr, L->E * h));
+    TRY_ALLOC(dalloc(&L->ex_loc, L->Tr * L->k));
+    TRY_ALLOC(dalloc(&L->gt_loc, L->Tr * L->k));
+    TRY_ALLOC(dalloc(&L->logits, L->Tr * L->E));
+    TRY_ALLOC(dalloc(&L->src, L->T));
+    TRY_ALLOC(dalloc(&L->dropped, L->T));
+    TRY_ALLOC(dalloc(reinterpret_cast<uint8_t**>(&L->perm_ws), permute_workspace_bytes(L->T, L->E, L->k, L->n)));
+    TRY_ALLOC(dalloc(&L->row_map_in, L->T * L->k));
+    TRY_ALLOC(dalloc(&L->out_expert, L->T * L->k));
+    TRY_ALLOC(dalloc(&L->out_src, L->T * L->k));
+    TRY_ALLOC(dalloc(&L->counts, L->E));
+    TRY_ALLOC(dalloc(&L->expert_off, el + 1));
+    TRY_ALLOC(dalloc(&L->rows, 1));
+    TRY_ALLOC(dalloc(&L->gpad_rows, el));
+    TRY_ALLOC(dalloc(&L->gpad_off, el + 1));
+    TRY_ALLOC(dalloc(&L->pad_tok, Mp));
+    TRY_ALLOC(dalloc(&L->row_dst, Mp));
+    TRY_ALLOC(dalloc(&L->row_gate, Mp));
+    TRY_ALLOC(dalloc(&L->x_perm, Mp * h));
+    TRY_ALLOC(dalloc(&L->fc1_out, Mp * 2 * f));
+    TRY_ALLOC(dalloc(&L->fc2_in, Mp * f));
+    TRY_ALLOC(dalloc(&L->dy_perm, Mp * h));
+    TRY_ALLOC(dalloc(&L->dfc1, Mp * 2 * f));
+    TRY_ALLOC(dalloc(&L->dgate_part, Mp * (f / 256)));
+    TRY_ALLOC(dalloc(&L->dlogits, L->Tr * L->E));
+    TRY_ALLOC(dalloc(&L->rw_part, ((L->Tr + kRwChunk - 1) / kRwChunk) * L->E * h));
+    TRY_ALLOC(dalloc(&L->t_x, L->n));
+    TRY_ALLOC(dalloc(&L->t_dy, L->n));
+    TRY_ALLOC(dalloc(&L->t_stage, L->n));
+    TRY_ALLOC(dalloc(&L->t_dstage, L->n));
+    TRY_ALLOC(dalloc(&L->t_ex, L->n));
+    TRY_ALLOC(dalloc(&L->t_gt, L->n));
+    TRY_ALLOC(dalloc(&L->t_dgate, L->n));
+    TRY_ALLOC(dalloc(&L->t_flags, L->n));
+    TRY_ALLOC(dalloc(&L->err, 1));
+    cudaMemset(L->err, 0, sizeof(int));
+    // zero the permuted buffers once so never-written rows are finite
+    cudaMemset(L->x_perm, 0, Mp * h * 2);
+    cudaMemset(L->dy_perm, 0, Mp * h * 2);
+    cudaMemset(L->fc2_in, 0, Mp * f * 2);
+    source_rank_kernel<<<64, 256>>>(L->src, (int)L->T, (int)L->Tr);
+    count_launch();
+    if (L->n == 1) {
+        TRY_ALLOC(fill_tables(L));
+        L->ipc_ready = true;
+    }
+    TRY_ALLOC(build_plans(L));
+    for (int i = 0; i < PH_COUNT; ++i) cudaEventCreate(&L->ev[i]);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+        moe_layer_destroy(L);
+        return set_error(MOE_ERR_CUDA, "layer init failed");
+    }
+#undef TRY_ALLOC
+    *out = L;
+    return MOE_OK;
+}
+
+void moe_layer_destroy(moe_layer* L) {
+    if (!L) return;
+    cudaDeviceSynchronize();
+    for (int p = 0; p < (int)L->peer_arena.size(); ++p)
+        if (p != L->rank && L->peer_arena[p]) cudaIpcCloseMemHandle(L->peer_arena[p]);
+    void* bufs[] = {L->arena, L->w1p, L->w2, L->wr, L->ex_loc, L->gt_loc, L->logits, L->src,
+                    L->dropped, L->perm_ws, L->row_map_in, L->out_expert, L->out_src, L->counts,
+                    L->expert_off, L->rows, L->gpad_rows, L->gpad_off, L->pad_tok, L->row_dst,
+                    L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
+                    L->dgate_part, L->dlogits, L->rw_part, L->t_x, L->t_dy, L->t_stage, L->t_dstage, L->t_ex,
+                    L->t_gt, L->t_dgate, L->t_flags, L->err};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    for (int i = 0; i < PH_COUNT; ++i)
+        if (L->ev[i]) cudaEventDestroy(L->ev[i]);
+    delete L;
+}
+
+moe_status moe_layer_set_weights(moe_layer* L, const uint16_t* d_w1, const uint16_t* d_w2,
+                                 const uint16_t* d_wr, moe_stream_t stream) {
+    MOE_CHECK_ARG(L && d_w1 && d_w2, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    pack_w1_kernel<<<kNumSMs * 4, 256, 0, s>>>(d_w1, L->w1p, (int)L->el, (int)L->f, (int)L->h);
+    count_launch();
+    MOE_CUDA_TRY(cudaGetLastError());
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->w2, d_w2, L->el * L->h * L->f * 2, cudaMemcpyDeviceToDevice, s));
+    if (d_wr) MOE_CUDA_TRY(cudaMemcpyAsync(L->wr, d_wr, L->E * L->h * 2, cudaMemcpyDeviceToDevice, s));
+    L->weights_set = true;
+    return MOE_OK;
+}
+
+uint16_t* moe_layer_input_buffer(moe_layer* L) { return L ? L->x_sym() : nullptr; }
+
+moe_status moe_layer_set_routing(moe_layer* L, const int32_t* d_experts, const float* d_gates,
+                                 moe_stream_t stream) {
+    MOE_CHECK_ARG(L && d_experts && d_gates, "null argument");
+    MOE_CHECK_ARG(L->cfg.route_mode == 1, "set_routing requires route_mode = 1 (injected)");
+    cudaStream_t s = (cudaStream_t)stream;
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->ex_loc, d_experts, L->Tr * L->k * 4, cudaMemcpyDeviceToDevice, s));
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->gt_loc, d_gates, L->Tr * L->k * 4, cudaMemcpyDeviceToDevice, s));
+    L->routing_set = true;
+    return MOE_OK;
+}
+
+moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, moe_stream_t stream) {
+    MOE_CHECK_ARG(L && d_y, "null argument");
+    MOE_CHECK_ARG(L->weights_set, "weights not set");
+    MOE_CHECK_ARG(L->cfg.route_mode == 0 || L->routing_set, "injected routing not set");
+    MOE_CHECK_ARG(L->n == 1 || L->ipc_ready, "ep_size > 1 requires moe_layer_ipc_import");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
+    for (int i = 0; i < PH_COUNT; ++i) L->ev_used[i] = false;
+    L->mark(PH_ROUTE, s);
+    if (d_x && d_x != L->x_sym())
+        MOE_CUDA_TRY(cudaMemcpyAsync(L->x_sym(), d_x, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
+    // K1 router (learned mode)
+    if (L->cfg.route_mode == 0) {
+        const size_t wbytes = (size_t)L->E * h * 2;
+        if (wbytes <= 200 * 1024) {
+            if (!L->router_attr) {
+                MOE_CUDA_TRY(cudaFuncSetAttribute(router_logits_smem_kernel,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                L->router_attr = true;
+            }
+            router_logits_smem_kernel<<<kNumSMs, 512, wbytes, s>>>(L->x_sym(), L->wr, (int)Tr, (int)h,
+                                                                   (int)L->E, L->logits);
+            count_launch();
+            MOE_TRY(launch_topk_from_logits(L->logits, Tr, L->E, k, L->ex_loc, L->gt_loc, s));
+        } else {
+            MOE_TRY(launch_router_topk(L->x_sym(), L->wr, Tr, h, L->E, k, L->logits, L->ex_loc,
+                                       L->gt_loc, s));
+        }
+    }
+    // routing metadata all-gather over NVLink
+    ++L->epoch;
+    publish_meta_kernel<<<std::min<int64_t>((Tr * k + 255) / 256, 64), 256, 0, s>>>(
+        L->ex_loc, L->gt_loc, (int)(Tr * k), (int)(L->rank * Tr * k), L->t_ex, L->t_gt, (int)L->n);
+    count_launch();
+    MOE_TRY(barrier(L, 0, s));
+    L->mark(PH_PERMUTE, s);
+    // K2: capacity drop (replicated on every rank over the global order) + permutation
+    if (L->cfg.capacity_factor > 0.0)
+        MOE_TRY(launch_capacity_drop(L->ex_all(), L->T, L->E, k, L->n, L->cfg.capacity_factor,
+                                     L->dropped, s));
+    else
+        MOE_CUDA_TRY(cudaMemsetAsync(L->dropped, 0, L->T, s));
+    MOE_TRY(launch_permute(L->ex_all(), L->src, L->dropped, L->T, L->E, k, L->n, L->rank, L->n,
+                           L->row_map_in, L->counts, L->out_expert, L->out_src, L->expert_off,
+                           L->rows, L->perm_ws, L->gpad_rows, L->gpad_off, L->pad_tok, 128, s));
+    row_info_kernel<<<(unsigned)el, 256, 0, s>>>(L->gpad_off, L->gpad_rows, L->expert_off,
+                                                 L->pad_tok, L->gt_all(), (int)k, (int)Tr,
+                                                 L->row_gate, L->row_dst);
+    count_launch();
+    // dispatch: AG + local scatter (rows pulled from the owning rank)
+    L->mark(PH_DISPATCH, s);
+    dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
+                                                     (int)Tr, (int)h, L->t_x, L->x_perm);
+    count_launch();
+    MOE_CUDA_TRY(cudaGetLastError());
+    // fc1 + SwiGLU (+ gate before fc2)
+    L->mark(PH_FC1, s);
+    const bool gate_before = L->cfg.gate_order == MOE_GATE_BEFORE_FC2;
+    {
+        GemmArgs a{};
+        a.G = (int)el;
+        a.group_rows = L->gpad_rows;
+        a.N = (int)(2 * f);
+        a.K = (int)h;
+        a.b_group_stride = (int)(2 * f);
+        a.out = L->fc1_out;
+        a.ldo = 2 * f;
+        a.out2 = L->fc2_in;
+        a.ldo2 = f;
+        a.row_gate = gate_before ? L->row_gate : nullptr;
+        MOE_TRY(gemm_launch(L->p_fc1, a, s));
+    }
+    // fc2 + gather to the source rank's combine staging
+    L->mark(PH_FC2, s);
+    {
+        GemmArgs a{};
+        a.G = (int)el;
+        a.group_rows = L->gpad_rows;
+        a.N = (int)h;
+        a.K = (int)f;
+        a.b_group_stride = (int)h;
+        a.ldo = h;
+        a.row_dst = L->row_dst;
+        a.rank_base = L->t_stage;
+        a.row_gate = L->row_gate;
+        a.gate_rows = gate_before ? 0 : 1;
+        MOE_TRY(gemm_launch(L->p_fc2, a, s));
+    }
+    MOE_TRY(barrier(L, 1, s));
+    // combine: fixed-order fp32 reduce over the k slots
+    L->mark(PH_COMBINE, s);
+    combine_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->stage_sym(), L->dropped + L->rank * Tr,
+                                                      (int)Tr, (int)k, (int)h, d_y, nullptr,
+                                                      nullptr, nullptr, nullptr, nullptr, 0);
+    count_launch();
+    MOE_CUDA_TRY(cudaGetLastError());
+    L->mark(PH_FWD_END, s);
+    L->fwd_done = true;
+    return MOE_OK;
+}
+
+moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx, uint16_t* d_dw1,
+                              uint16_t* d_dw2, float* d_dwr, moe_stream_t stream) {
+    MOE_CHECK_ARG(L && d_dy && d_dx, "null argument");
+    MOE_CHECK_ARG(L->fwd_done, "backward needs a preceding forward");
+    if (L->cfg.gate_order != MOE_GATE_BEFORE_FC2)
+        return set_error(MOE_ERR_UNSUPPORTED, "backward implemented for gate_order = before_fc2");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
+    L->mark(PH_DISPATCH_DY, s);
+    if (d_dy != L->dy_sym())
+        MOE_CUDA_TRY(cudaMemcpyAsync(L->dy_sym(), d_dy, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
+    // dgates of dropped (token, slot)s are never written by an expert rank
+    MOE_CUDA_TRY(cudaMemsetAsync(L->dgate_sym(), 0, Tr * k * 4, s));
+    ++L->epoch;
+    MOE_TRY(barrier(L, 2, s));
+    // AG(dy) + scatter into permuted order
+    dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
+                                                     (int)Tr, (int)h, L->t_dy, L->dy_perm);
+    count_launch();
+    // fc2 dgrad fused with SwiGLU/gate backward and remat of fc2_in
+    L->mark(PH_FC2_DGRAD, s);
+    {
+        GemmArgs a{};
+        a.G = (int)el;
+        a.group_rows = L->gpad_rows;
+        a.N = (int)f;
+        a.K = (int)h;
+        a.b_group_stride = (int)h;
+        a.out = L->dfc1;
+        a.ldo = 2 * f;
+        a.out2 = L->fc2_in;
+        a.ldo2 = f;
+        a.aux = L->fc1_out;
+        a.ld_aux = 2 * f;
+        a.row_gate = L->row_gate;
+        a.row_part = L->dgate_part;
+        MOE_TRY(gemm_launch(L->p_fc2_dgrad, a, s));
+    }
+    L->mark(PH_FC2_WGRAD, s);
+    if (d_dw2) {
+        GemmArgs a{};
+        a.G = (int)el;
+        a.group_rows = L->gpad_rows;
+        a.N = (int)f;
+        a.K = (int)h;  // output rows per expert
+        a.out = d_dw2;
+        a.ldo = f;
+        MOE_TRY(gemm_launch(L->p_fc2_wgrad, a, s));
+    }
+    L->mark(PH_FC1_DGRAD, s);
+    {
+        GemmArgs a{};
+        a.G = (int)el;
+        a.group_rows = L->gpad_rows;
+        a.N = (int)h;
+        a.K = (int)(2 * f);
+        a.b_group_stride = (int)(2 * f);
+        a.ldo = h;
+        a.row_dst = L->row_dst;
+        a.rank_base = L->t_dstage;
+        MOE_TRY(gemm_launch(L->p_fc1_dgrad, a, s));
+    }
+    L->mark(PH_FC1_WGRAD, s);
+    if (d_dw1) {
+        GemmArgs a{};
+        a.G = (int)el;
+        a.group_rows = L->gpad_rows;
+        a.N = (int)h;
+        a.K = (int)(2 * f);
+        a.out = d_dw1;
+        a.ldo = h;
+        a.interleave_rows = 1;
+        MOE_TRY(gemm_launch(L->p_fc1_wgrad, a, s));
+    }
+    L->mark(PH_DGATE, s);
+    dgate_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgate_part, (int)(f / 256), L->row_dst,
+                                                L->gpad_off + el, L->t_dgate);
+    count_launch();
+    MOE_TRY(barrier(L, 3, s));
+    L->mark(PH_COMBINE_DX, s);
+    const bool router = L->cfg.route_mode == 0;
+    combine_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(
+        L->dstage_sym(), L->dropped + L->rank * Tr, (int)Tr, (int)k, (int)h, d_dx,
+        router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
+        router ? L->dgate_sym() : nullptr, router ? L->wr : nullptr,
+        router ? L->dlogits : nullptr, (int)L->E);
+    count_launch();
+    L->mark(PH_ROUTER_WGRAD, s);
+    if (d_dwr) {
+        if (router) {
+            const int nch = (int)((Tr + kRwChunk - 1) / kRwChunk);
+            if (L->E <= 8)
+                router_wgrad_partial_kernel<8><<<dim3((unsigned)((h + 255) / 256), nch), 256, 0, s>>>(
+                    L->dlogits, L->x_sym(), (int)Tr, (int)h, (int)L->E, L->rw_part);
+            else
+                router_wgrad_partial_kernel<32><<<dim3((unsigned)((h + 255) / 256), nch), 256, 0, s>>>(
+                    L->dlogits, L->x_sym(), (int)Tr, (int)h, (int)L->E, L->rw_part);
+            router_wgrad_reduce_kernel<<<kNumSMs * 2, 256, 0, s>>>(L->rw_part, nch, (int)L->E,
+                                                                   (int)h, d_dwr);
+            count_launch(2);
+        } else {
+            MOE_CUDA_TRY(cudaMemsetAsync(d_dwr, 0, L->E * h * 4, s));
+        }
+    }
+    MOE_CUDA_TRY(cudaGetLastError());
+    L->mark(PH_END, s);
+    return MOE_OK;
+}
+
+moe_status moe_layer_routing(moe_layer* L, moe_layer_routing_view* v) {
+    MOE_CHECK_ARG(L && v, "null argument");
+    v->experts = L->ex_all();
+    v->gates = L->gt_all();
+    v->dropped = L->dropped;
+    v->row_map_in = L->row_map_in;
+    v->per_expert_counts = L->counts;
+    v->out_expert = L->out_expert;
+    v->out_source_rank = L->out_src;
+    v->rows = L->rows;
+    v->dgates = L->dgate_sym();
+    v->logits = L->logits;
+    return MOE_OK;
+}
+
+moe_status moe_layer_enable_timing(moe_layer* L, int enable) {
+    MOE_CHECK_ARG(L, "null argument");
+    L->timing = enable != 0;
+    return MOE_OK;
+}
+
+moe_status moe_layer_phase_times(moe_layer* L, float* h_ms, int max_phases, int* n_phases,
+                                 const char** names) {
+    MOE_CHECK_ARG(L && h_ms && n_phases, "null argument");
+    int last = -1;
+    for (int i = 0; i < PH_COUNT; ++i)
+        if (L->ev_used[i]) last = i;
+    if (last < 0) return set_error(MOE_ERR_INVALID, "no timed phases recorded");
+    MOE_CUDA_TRY(cudaEventSynchronize(L->ev[last]));
+    int cnt = 0;
+    for (int i = 0; i < PH_END && cnt < max_phases; ++i) {
+        if (!L->ev_used[i] || i == PH_FWD_END) continue;
+        int j = i + 1;
+        while (j < PH_COUNT && !L->ev_used[j]) ++j;
+        if (i == PH_COMBINE) j = PH_FWD_END;
+        if (j >= PH_COUNT) break;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, L->ev[i], L->ev[j]);
+        h_ms[cnt] = ms;
+        if (names) names[cnt] = kPhaseNames[i];
+        ++cnt;
+    }
+    *n_phases = cnt;
+    return MOE_OK;
+}
+
+size_t moe_layer_ipc_handle_size(void) { return sizeof(cudaIpcMemHandle_t); }
+
+moe_status moe_layer_ipc_export(moe_layer* L, void* h_blob) {
+    MOE_CHECK_ARG(L && h_blob, "null argument");
+    cudaIpcMemHandle_t hdl;
+    MOE_CUDA_TRY(cudaIpcGetMemHandle(&hdl, L->arena));
+    std::memcpy(h_blob, &hdl, sizeof(hdl));
+    return MOE_OK;
+}
+
+moe_status moe_layer_ipc_import(moe_layer* L, const void* h_blobs) {
+    MOE_CHECK_ARG(L && h_blobs, "null argument");
+    const auto* hs = static_cast<const cudaIpcMemHandle_t*>(h_blobs);
+    for (int p = 0; p < (int)L->n; ++p) {
+        if (p == L->rank) continue;
+        void* ptr = nullptr;
+        MOE_CUDA_TRY(cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess));
+        L->peer_arena[p] = static_cast<uint8_t*>(ptr);
+    }
+    MOE_TRY(fill_tables(L));
+    L->ipc_ready = true;
+    return MOE_OK;
+}
+
+int moe_layer_error_flag(moe_layer* L) {
+    int v = 0;
+    if (L && L->err) cudaMemcpy(&v, L->err, sizeof(int), cudaMemcpyDeviceToHost);
+    return v;
+}
+
+}  // extern "C"

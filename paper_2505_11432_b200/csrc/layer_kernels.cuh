@@ -1,0 +1,309 @@
+// layer_kernels.cuh — the memory-bound operators of the MoE layer around
+// the grouped GEMMs: permuted-row metadata, dispatch (AG + local scatter),
+// combine (gather + reduce), SwiGLU/gate backward reductions, router
+// backward, weight packing and the cross-GPU flag barrier.
+//
+// Reference operator nodes (graph.cpp): scatter :276-286, gather :302-306,
+// weighted_sum :292-295, router :268-271, collectives ag_ffn_in/rs_ffn_out
+// :276-310. All of these are HBM- or NVLink-bound; kernels use 16-byte
+// vector accesses, one warp per row, grids sized to the SM count.
+#pragma once
+
+#include "common.cuh"
+
+namespace moe {
+
+// Per padded permuted row: source token-slot, gate, combine destination.
+// Grid: one block per local expert.
+__global__ void row_info_kernel(const int32_t* __restrict__ group_pad_off,
+                                const int32_t* __restrict__ group_pad_rows,
+                                const int32_t* __restrict__ expert_offsets,
+                                int32_t* __restrict__ pad_row_tok,  // in: real rows; out: -1 pads
+                                const float* __restrict__ gates_all, int k, int tokens_per_rank,
+                                float* __restrict__ row_gate, int32_t* __restrict__ row_dst) {
+    const int g = blockIdx.x;
+    const int poff = group_pad_off[g], pr = group_pad_rows[g];
+    const int cnt = expert_offsets[g + 1] - expert_offsets[g];
+    for (int r = threadIdx.x; r < pr; r += blockDim.x) {
+        const int pp = poff + r;
+        if (r < cnt) {
+            const int i = pad_row_tok[pp];  // t*k + slot (global token id)
+            const int t = i / k, slot = i - t * k;
+            const int src = t / tokens_per_rank;
+            row_gate[pp] = gates_all[i];
+            row_dst[pp] = (src << 27) | ((t - src * tokens_per_rank) * k + slot);
+        } else {
+            pad_row_tok[pp] = -1;
+            row_gate[pp] = 0.0f;
+            row_dst[pp] = -1;
+        }
+    }
+}
+
+// Dispatch: dst[pp, :] = src_rank_buffer[t_local, :] for real rows, 0 for
+// pads (AG + local scatter fused: rows are pulled straight from the owning
+// rank's buffer over NVLink into permuted order).
+// One warp per row, 16-byte vectors, 4 in flight per lane.
+__global__ void dispatch_rows_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad,
+                                     int k, int tokens_per_rank, int h,
+                                     const uint16_t* const* __restrict__ src_bufs,
+                                     uint16_t* __restrict__ dst) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int total = *nrows_pad;
+    const int nvec = h / 8;
+    for (int pp = warp; pp < total; pp += nwarps) {
+        const int i = pad_row_tok[pp];
+        uint4* d = reinterpret_cast<uint4*>(dst + (int64_t)pp * h);
+        if (i < 0) {
+            for (int v = lane; v < nvec; v += 32) d[v] = make_uint4(0, 0, 0, 0);
+            continue;
+        }
+        const int t = i / k;
+        const int src = t / tokens_per_rank;
+        const uint4* s = reinterpret_cast<const uint4*>(src_bufs[src] + (int64_t)(t - src * tokens_per_rank) * h);
+        int v = lane;
+        for (; v + 96 < nvec; v += 128) {
+            const uint4 a0 = s[v], a1 = s[v + 32], a2 = s[v + 64], a3 = s[v + 96];
+            d[v] = a0; d[v + 32] = a1; d[v + 64] = a2; d[v + 96] = a3;
+        }
+        for (; v < nvec; v += 32) d[v] = s[v];
+    }
+}
+
+// Router backward helper: given gates g (softmax over the k selected logits)
+// and dgates, dlogit_j = g_j (dg_j - sum_i g_i dg_i).
+__device__ __forceinline__ void softmax_topk_bwd(const float* g, const float* dg, int k, float* dl) {
+    float s = 0.0f;
+    for (int j = 0; j < k; ++j) s += g[j] * dg[j];
+    for (int j = 0; j < k; ++j) dl[j] = g[j] * (dg[j] - s);
+}
+
+// Combine: y[t, :] = sum over slots (fixed slot order, fp32) of the staged
+// expert outputs (a2a_fp32 semantics, numerics.cpp:172-192); dropped tokens
+// produce 0. Optional router term for dx: += sum_j dlogit_j * wr[e_j, :].
+// One warp per token; each lane owns 8-column groups.
+__global__ void combine_reduce_kernel(const uint16_t* __restrict__ stage, const uint8_t* __restrict__ dropped,
+                                      int T, int k, int h, uint16_t* __restrict__ out,
+                                      const int32_t* __restrict__ experts, const float* __restrict__ gates,
+                                      const float* __restrict__ dgates, const uint16_t* __restrict__ wr,
+                                      float* __restrict__ dlogits, int E) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int nvec = h / 8;
+    for (int t = warp; t < T; t += nwarps) {
+        uint4* o = reinterpret_cast<uint4*>(out + (int64_t)t * h);
+        if (dropped && dropped[t]) {
+            for (int v = lane; v < nvec; v += 32) o[v] = make_uint4(0, 0, 0, 0);
+            if (dlogits && lane < E) for (int e = lane; e < E; e += 32) dlogits[(int64_t)t * E + e] = 0.0f;
+            continue;
+        }
+        float dl[8];
+        int ex[8];
+        const bool router = wr != nullptr;
+        if (router) {
+            float g[8], dg[8];
+            for (int j = 0; j < k; ++j) {
+                g[j] = gates[(int64_t)t * k + j];
+                dg[j] = dgates[(int64_t)t * k + j];
+                ex[j] = experts[(int64_t)t * k + j];
+            }
+            softmax_topk_bwd(g, dg, k, dl);
+            if (dlogits) {
+                for (int e = lane; e < E; e += 32) {
+                    float v = 0.0f;
+                    for (int j = 0; j < k; ++j) v = (ex[j] == e) ? dl[j] : v;
+                    dlogits[(int64_t)t * E + e] = v;
+                }
+            }
+        }
+        for (int v = lane; v < nvec; v += 32) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int j = 0; j < k; ++j) {
+                const uint4 sv = reinterpret_cast<const uint4*>(stage + ((int64_t)t * k + j) * h)[v];
+                const float2 p0 = unpack_bf16x2(sv.x), p1 = unpack_bf16x2(sv.y),
+                             p2 = unpack_bf16x2(sv.z), p3 = unpack_bf16x2(sv.w);
+                acc[0] += p0.x; acc[1] += p0.y; acc[2] += p1.x; acc[3] += p1.y;
+                acc[4] += p2.x; acc[5] += p2.y; acc[6] += p3.x; acc[7] += p3.y;
+            }
+            if (router) {
+                for (int j = 0; j < k; ++j) {
+                    const uint4 wv = reinterpret_cast<const uint4*>(wr + (int64_t)ex[j] * h)[v];
+                    const float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y),
+                                 w2 = unpack_bf16x2(wv.z), w3 = unpack_bf16x2(wv.w);
+                    acc[0] += dl[j] * w0.x; acc[1] += dl[j] * w0.y; acc[2] += dl[j] * w1.x; acc[3] += dl[j] * w1.y;
+                    acc[4] += dl[j] * w2.x; acc[5] += dl[j] * w2.y; acc[6] += dl[j] * w3.x; acc[7] += dl[j] * w3.y;
+                }
+            }
+            o[v] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                              pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+        }
+    }
+}
+
+// dgate of each permuted row = sum over f-tiles of the epilogue partials
+// (fixed order, deterministic), scattered to (source rank, t_local*k+slot).
+__global__ void dgate_reduce_kernel(const float* __restrict__ part, int n_parts,
+                                    const int32_t* __restrict__ row_dst, const int32_t* nrows_pad,
+                                    float* const* __restrict__ dst_bufs) {
+    const int total = *nrows_pad;
+    for (int pp = blockIdx.x * blockDim.x + threadIdx.x; pp < total; pp += gridDim.x * blockDim.x) {
+        const int d = row_dst[pp];
+        if (d < 0) continue;
+        float s = 0.0f;
+        for (int q = 0; q < n_parts; ++q) s += part[(int64_t)pp * n_parts + q];
+        dst_bufs[d >> 27][d & ((1 << 27) - 1)] = s;
+    }
+}
+
+// Router weight gradient dwr[e, c] = sum_t dlogits[t, e] * x[t, c] (fp32).
+// Pass 1: block (column tile of 256, token chunk of 128) -> partial [chunk][E][h];
+// pass 2: fixed-order sum over chunks (deterministic). E <= 32 per pass.
+constexpr int kRwChunk = 128;
+template <int EB>
+__global__ void router_wgrad_partial_kernel(const float* __restrict__ dlogits, const uint16_t* __restrict__ x,
+                                            int T, int h, int E, float* __restrict__ part) {
+    __shared__ float s_dl[kRwChunk * EB];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t0 = blockIdx.y * kRwChunk;
+    const int nt = min(kRwChunk, T - t0);
+    for (int e0 = 0; e0 < E; e0 += EB) {
+        const int ne = min(EB, E - e0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < nt * EB; i += blockDim.x) {
+            const int tt = i / EB, ee = i % EB;
+            s_dl[i] = ee < ne ? dlogits[(int64_t)(t0 + tt) * E + e0 + ee] : 0.0f;
+        }
+        __syncthreads();
+        float acc[EB];
+#pragma unroll
+        for (int q = 0; q < EB; ++q) acc[q] = 0.0f;
+        if (c < h) {
+            for (int tt = 0; tt < nt; ++tt) {
+                const float xv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(x)[(int64_t)(t0 + tt) * h + c]);
+#pragma unroll
+                for (int q = 0; q < EB; ++q) acc[q] = fmaf(s_dl[tt * EB + q], xv, acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < EB; ++q)
+                if (q < ne) part[((int64_t)blockIdx.y * E + e0 + q) * h + c] = acc[q];
+        }
+    }
+}
+
+__global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int nchunks, int E, int h,
+                                           float* __restrict__ dwr) {
+    const int64_t n = (int64_t)E * h;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int q = 0; q < nchunks; ++q) s += part[(int64_t)q * n + i];
+        dwr[i] = s;
+    }
+}
+
+// Pack w1 [el][2f][h] ([a | b] rows) into the interleaved layout the fused
+// SwiGLU epilogue expects: per 256-row block, 128 a-rows then 128 b-rows.
+__global__ void pack_w1_kernel(const uint16_t* __restrict__ w1, uint16_t* __restrict__ w1p, int el,
+                               int f, int h) {
+    const int64_t rows = (int64_t)el * 2 * f;
+    const int nvec = h / 8;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int e = (int)(r / (2 * f));
+        const int j = (int)(r % (2 * f));
+        const int blk = j >> 8, w = j & 255;
+        const int src_j = w < 128 ? blk * 128 + w : f + blk * 128 + (w - 128);
+        const uint4* s = reinterpret_cast<const uint4*>(w1 + ((int64_t)e * 2 * f + src_j) * h);
+        uint4* d = reinterpret_cast<uint4*>(w1p + r * h);
+        for (int v = threadIdx.x; v < nvec; v += blockDim.x) d[v] = s[v];
+    }
+}
+
+// Copy this rank's routing (experts/gates for its T_r tokens) into every
+// rank's global routing table at offset rank*T_r*k.
+__global__ void publish_meta_kernel(const int32_t* __restrict__ ex, const float* __restrict__ gt,
+                                    int count, int offset, int32_t* const* ex_bufs,
+                                    float* const* gt_bufs, int n) {
+    for (int p = 0; p < n; ++p)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+            ex_bufs[p][offset + i] = ex[i];
+            gt_bufs[p][offset + i] = gt[i];
+        }
+}
+
+// Device-side barrier over NVLink: rank r stores `epoch` into slot[r] of
+// every peer's flag array (release, system scope), then waits until its own
+// array holds >= epoch for all peers. Bounded spin -> *err = 1 on timeout.
+__global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot, int n, int rank,
+                                    uint32_t epoch, unsigned long long timeout_ns, int* err) {
+    const int i = threadIdx.x;
+    if (i < n) {
+        __threadfence_system();
+        st_release_sys(peer_flags[i] + slot * 64 + rank, epoch);
+    }
+    __syncthreads();
+    if (i < n) {
+        const uint32_t* mine = peer_flags[rank] + slot * 64 + i;
+        const uint64_t t0 = globaltimer();
+        while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
+            if (globaltimer() - t0 > timeout_ns) {
+                atomicExch(err, 1);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// K1 fast path: router weights staged in shared memory (E*h*2 <= ~200 KB),
+// one warp per token, x streamed with 16-byte loads.
+__global__ void router_logits_smem_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr,
+                                          int T, int h, int E, float* __restrict__ logits) {
+    extern __shared__ __align__(16) uint8_t s_raw[];
+    uint4* s_w = reinterpret_cast<uint4*>(s_raw);
+    const int nvec = h / 8;
+    for (int i = threadIdx.x; i < E * nvec; i += blockDim.x) s_w[i] = reinterpret_cast<const uint4*>(wr)[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int t = blockIdx.x * wpb + warp; t < T; t += gridDim.x * wpb) {
+        const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)t * h);
+        for (int e0 = 0; e0 < E; e0 += 8) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int v = lane; v < nvec; v += 32) {
+                const uint4 xv = __ldg(xr + v);
+                const float2 x0 = unpack_bf16x2(xv.x), x1 = unpack_bf16x2(xv.y),
+                             x2 = unpack_bf16x2(xv.z), x3 = unpack_bf16x2(xv.w);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (e0 + q < E) {
+                        const uint4 wv = s_w[(e0 + q) * nvec + v];
+                        const float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y),
+                                     w2 = unpack_bf16x2(wv.z), w3 = unpack_bf16x2(wv.w);
+                        float a = acc[q];
+                        a = fmaf(x0.x, w0.x, a); a = fmaf(x0.y, w0.y, a);
+                        a = fmaf(x1.x, w1.x, a); a = fmaf(x1.y, w1.y, a);
+                        a = fmaf(x2.x, w2.x, a); a = fmaf(x2.y, w2.y, a);
+                        a = fmaf(x3.x, w3.x, a); a = fmaf(x3.y, w3.y, a);
+                        acc[q] = a;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                float a = acc[q];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+                if (lane == 0 && e0 + q < E) logits[(int64_t)t * E + e0 + q] = a;
+            }
+        }
+    }
+}
+
+__global__ void source_rank_kernel(int32_t* src, int T, int tokens_per_rank) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
+        src[t] = t / tokens_per_rank;
+}
+
+}  // namespace moe

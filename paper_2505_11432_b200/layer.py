@@ -1,0 +1,166 @@
+"""MoE layer (reference operator chain ffn_norm? -> router -> dispatch ->
+fc1 -> swiglu -> weighted_sum -> fc2 -> gather/combine, graph.cpp:254-311,
+and its backward, graph.cpp:333-401) as a handle over the C ABI.
+
+Multi-GPU: one process per GPU; `MoELayer.connect(group)` exchanges the
+CUDA-IPC handles of every rank's symmetric arena over torch.distributed, after
+which dispatch/combine run as in-kernel NVLink loads/stores.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import DomainError, check, i64, lib, ptr, require_cuda, stream_ptr
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("tokens_per_rank", C.c_int64), ("hidden", C.c_int64), ("ffn_hidden", C.c_int64),
+                ("num_experts", C.c_int64), ("top_k", C.c_int64), ("ep_size", C.c_int64),
+                ("rank", C.c_int64), ("capacity_factor", C.c_double), ("gate_order", C.c_int32),
+                ("comm_format", C.c_int32), ("ep_pattern", C.c_int32), ("route_mode", C.c_int32)]
+
+
+class _RoutingView(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("experts", "gates", "dropped", "row_map_in",
+                                          "per_expert_counts", "out_expert", "out_source_rank",
+                                          "rows", "dgates", "logits")]
+
+
+class _DevArray:
+    """Zero-copy view of layer-owned device memory (CUDA array interface)."""
+
+    def __init__(self, p, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(p), False), "version": 3, "strides": None}
+
+
+def _view(p, shape, dtype):
+    typestr = {torch.int32: "<i4", torch.float32: "<f4", torch.uint8: "|u1",
+               torch.bfloat16: "<u2"}[dtype]
+    t = torch.as_tensor(_DevArray(p, shape, typestr), device="cuda")
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+
+
+GATE_ORDERS = {"before_fc2_in": 0, "before_fc2": 0, "after_fc2_out": 1, "after_fc2": 1}
+
+
+class MoELayer:
+    def __init__(self, tokens_per_rank: int, hidden: int, ffn_hidden: int, num_experts: int,
+                 top_k: int, ep_size: int = 1, rank: int = 0, capacity_factor: float = 0.0,
+                 gate_order: str = "before_fc2_in", comm_format: str = "bf16",
+                 route_mode: str = "learned"):
+        cfg = _Cfg(tokens_per_rank, hidden, ffn_hidden, num_experts, top_k, ep_size, rank,
+                   float(capacity_factor), GATE_ORDERS[gate_order],
+                   {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}[comm_format], 0,
+                   {"learned": 0, "injected": 1}[route_mode])
+        self.cfg = cfg
+        self.Tr, self.h, self.f, self.E, self.k = tokens_per_rank, hidden, ffn_hidden, num_experts, top_k
+        self.n, self.rank = ep_size, rank
+        self.el = num_experts // ep_size
+        h_ = C.c_void_p()
+        check(lib().moe_layer_create(C.byref(cfg), C.byref(h_)))
+        self._h = h_
+        self._x_in = _view(lib().moe_layer_input_buffer(self._h), (tokens_per_rank, hidden), torch.bfloat16)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().moe_layer_destroy(h)
+            self._h = None
+
+    # ------------------------------------------------------------------
+    @property
+    def input_buffer(self) -> torch.Tensor:
+        """[T_r, h] bf16 view of the layer's symmetric input buffer."""
+        return self._x_in
+
+    def set_weights(self, w1: torch.Tensor, w2: torch.Tensor, wr: torch.Tensor | None = None, stream=None):
+        """w1 [E_local, 2f, h] ([a | b] rows), w2 [E_local, h, f], wr [E, h]; bf16."""
+        require_cuda(w1, w2, wr)
+        if w1.shape != (self.el, 2 * self.f, self.h) or w2.shape != (self.el, self.h, self.f):
+            raise DomainError("weight shapes must be w1 [E/n, 2f, h], w2 [E/n, h, f]")
+        if wr is not None and wr.shape != (self.E, self.h):
+            raise DomainError("router weight must be [E, h]")
+        self._keep = (w1.contiguous(), w2.contiguous(), None if wr is None else wr.contiguous())
+        check(lib().moe_layer_set_weights(self._h, ptr(self._keep[0]), ptr(self._keep[1]),
+                                          ptr(self._keep[2]), stream_ptr(stream)))
+
+    def set_routing(self, experts: torch.Tensor, gates: torch.Tensor, stream=None):
+        require_cuda(experts, gates)
+        self._route_keep = (experts.to(torch.int32).contiguous(), gates.float().contiguous())
+        check(lib().moe_layer_set_routing(self._h, ptr(self._route_keep[0]), ptr(self._route_keep[1]),
+                                          stream_ptr(stream)))
+
+    def forward(self, x: torch.Tensor | None, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if x is not None:
+            require_cuda(x)
+            x = x.contiguous()
+        if y is None:
+            y = torch.empty(self.Tr, self.h, dtype=torch.bfloat16, device="cuda")
+        check(lib().moe_layer_forward(self._h, ptr(x), ptr(y), stream_ptr(stream)))
+        return y
+
+    def backward(self, dy: torch.Tensor, dx=None, dw1=None, dw2=None, dwr=None, want_weight_grads=True,
+                 stream=None):
+        require_cuda(dy)
+        dy = dy.contiguous()
+        if dx is None:
+            dx = torch.empty(self.Tr, self.h, dtype=torch.bfloat16, device="cuda")
+        if want_weight_grads:
+            if dw1 is None:
+                dw1 = torch.empty(self.el, 2 * self.f, self.h, dtype=torch.bfloat16, device="cuda")
+            if dw2 is None:
+                dw2 = torch.empty(self.el, self.h, self.f, dtype=torch.bfloat16, device="cuda")
+            if dwr is None:
+                dwr = torch.empty(self.E, self.h, dtype=torch.float32, device="cuda")
+        check(lib().moe_layer_backward(self._h, ptr(dy), ptr(dx), ptr(dw1), ptr(dw2), ptr(dwr),
+                                       stream_ptr(stream)))
+        return dx, dw1, dw2, dwr
+
+    def routing(self):
+        """Routing results of the last forward (device tensors)."""
+        v = _RoutingView()
+        check(lib().moe_layer_routing(self._h, C.byref(v)))
+        T = self.Tr * self.n
+        torch.cuda.synchronize()
+        rows = int(_view(v.rows, (1,), torch.int32).item())
+        return dict(
+            experts=_view(v.experts, (T, self.k), torch.int32),
+            gates=_view(v.gates, (T, self.k), torch.float32),
+            dropped=_view(v.dropped, (T,), torch.uint8),
+            row_map_in=_view(v.row_map_in, (max(rows, 1),), torch.int32)[:rows],
+            per_expert_counts=_view(v.per_expert_counts, (self.E,), torch.int32),
+            out_expert=_view(v.out_expert, (max(rows, 1),), torch.int32)[:rows],
+            out_source_rank=_view(v.out_source_rank, (max(rows, 1),), torch.int32)[:rows],
+            dgates=_view(v.dgates, (self.Tr, self.k), torch.float32),
+            logits=_view(v.logits, (self.Tr, self.E), torch.float32),
+        )
+
+    def enable_timing(self, on=True):
+        check(lib().moe_layer_enable_timing(self._h, int(on)))
+
+    def phase_times(self):
+        ms = (C.c_float * 32)()
+        names = (C.c_char_p * 32)()
+        cnt = C.c_int()
+        check(lib().moe_layer_phase_times(self._h, ms, 32, C.byref(cnt), names))
+        return {names[i].decode(): ms[i] for i in range(cnt.value)}
+
+    def error_flag(self) -> int:
+        return int(lib().moe_layer_error_flag(self._h))
+
+    # ------------------------------------------------------------------
+    def connect(self, group=None):
+        """Exchange IPC handles with every rank (collective over torch.distributed)."""
+        import torch.distributed as dist
+        sz = int(lib().moe_layer_ipc_handle_size())
+        blob = (C.c_uint8 * sz)()
+        check(lib().moe_layer_ipc_export(self._h, blob))
+        mine = bytes(blob)
+        allb = [None] * self.n
+        dist.all_gather_object(allb, mine, group=group)
+        joined = b"".join(allb)
+        buf = (C.c_uint8 * len(joined)).from_buffer_copy(joined)
+        check(lib().moe_layer_ipc_import(self._h, buf))

@@ -1,0 +1,98 @@
+"""MoE layer forward/backward on the GPU vs the fp32 CPU oracle.
+
+Tolerances (stated, per north_star): bf16 path rel-L2 <= 1e-2 per output
+tensor against the fp32 oracle evaluated on the same bf16-valued inputs and
+the GPU's own routing decisions; routing maps bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def make_layer(T, h, f, E, k, seed=0, route_mode="learned", cf=0.0):
+    from paper_2505_11432_b200.layer import MoELayer
+    g = torch.Generator().manual_seed(seed)
+    x = (torch.randn(T, h, generator=g) * 0.5).bfloat16()
+    w1 = (torch.randn(E, 2 * f, h, generator=g) / h ** 0.5).bfloat16()
+    w2 = (torch.randn(E, h, f, generator=g) / f ** 0.5).bfloat16()
+    wr = (torch.randn(E, h, generator=g) / h ** 0.5).bfloat16()
+    L = MoELayer(T, h, f, E, k, capacity_factor=cf, route_mode=route_mode)
+    L.set_weights(w1.cuda(), w2.cuda(), wr.cuda())
+    return L, x, w1, w2, wr
+
+
+@pytest.mark.parametrize("T,h,f,E,k", [(256, 512, 512, 8, 2), (384, 768, 1024, 4, 1), (512, 512, 768, 16, 4)])
+def test_layer_fwd_bwd_vs_oracle(T, h, f, E, k):
+    import pyoracle as P
+    L, x, w1, w2, wr = make_layer(T, h, f, E, k)
+    y = L.forward(x.cuda())
+    torch.cuda.synchronize()
+    r = L.routing()
+    ex = r["experts"].cpu().numpy()
+    gt = r["gates"].cpu().numpy()
+    dr = r["dropped"].cpu().numpy()
+    lg = r["logits"].cpu().numpy()
+    xf, w1f, w2f, wrf = (t.float().numpy() for t in (x, w1, w2, wr))
+    # router: logits match the fp32 oracle; selection consistent with logits
+    olg, oex, og = P.orc_router_topk(xf, wrf, k)
+    assert rel(lg, olg) < 1e-4
+    # routing maps bit-exact vs the oracle on the GPU's own assignment
+    m = P.orc_build_scatter_map(ex, np.zeros(T, np.int32), dr, E, 1, 0)
+    assert (r["row_map_in"].cpu().numpy() == m["row_map_in"]).all()
+    assert (r["per_expert_counts"].cpu().numpy() == m["per_expert_counts"]).all()
+    # forward
+    oy = P.orc_moe_forward(xf, ex, gt, dr, w1f, w2f)
+    assert rel(y.float().cpu().numpy(), oy) < TOL
+    # backward
+    dy = (torch.randn(T, h, generator=torch.Generator().manual_seed(7)) * 0.1).bfloat16()
+    dx, dw1, dw2, dwr = L.backward(dy.cuda())
+    torch.cuda.synchronize()
+    ob = P.orc_moe_backward(xf, dy.float().numpy(), ex, gt, lg, dr, w1f, w2f, wrf)
+    assert rel(L.routing()["dgates"].cpu().numpy(), ob["dgates"]) < TOL
+    assert rel(dx.float().cpu().numpy(), ob["dx"]) < TOL
+    assert rel(dw1.float().cpu().numpy(), ob["dw1"]) < TOL
+    assert rel(dw2.float().cpu().numpy(), ob["dw2"]) < TOL
+    assert rel(dwr.cpu().numpy(), ob["dwr"]) < TOL
+
+
+def test_layer_injected_routing_with_drops():
+    """Injected reference routing (Zipf) with capacity drops (cf=0.5) through the layer."""
+    import os
+    import pyoracle as P
+    from conftest import GOLDEN
+    g = np.load(os.path.join(GOLDEN, "routing_t_skewed_512_s11.npz"))
+    T, E, k = int(g["T"]), int(g["E"]), int(g["k"])
+    ex = g["experts"].astype(np.int32).reshape(T, k)
+    h, f = 512, 512
+    L, x, w1, w2, wr = make_layer(T, h, f, E, k, seed=3, route_mode="injected", cf=0.5)
+    # the capacity drop inside the layer runs with n_groups = ep_size = 1
+    gates = np.random.default_rng(0).random((T, k)).astype(np.float32)
+    gates /= gates.sum(1, keepdims=True)
+    L.set_routing(torch.from_numpy(ex).cuda(), torch.from_numpy(gates).cuda())
+    y = L.forward(x.cuda())
+    torch.cuda.synchronize()
+    r = L.routing()
+    want_dr = P.orc_capacity_drop(ex, E, 1, 0.5)
+    assert want_dr.sum() > 0
+    assert (r["dropped"].cpu().numpy() == want_dr).all()
+    oy = P.orc_moe_forward(x.float().numpy(), ex, gates, want_dr, w1.float().numpy(), w2.float().numpy())
+    assert rel(y.float().cpu().numpy(), oy) < TOL
+    dy = (torch.randn(T, h) * 0.1).bfloat16()
+    dx, dw1, dw2, _ = L.backward(dy.cuda())
+    ob = P.orc_moe_backward(x.float().numpy(), dy.float().numpy(), ex, gates, np.zeros((T, E), np.float32),
+                            want_dr, w1.float().numpy(), w2.float().numpy(), wr.float().numpy())
+    # injected gates are constants: the oracle's router term is the only
+    # difference; compare dx without it via dW only, plus dgates
+    assert rel(dw1.float().cpu().numpy(), ob["dw1"]) < TOL
+    assert rel(dw2.float().cpu().numpy(), ob["dw2"]) < TOL
+    assert rel(L.routing()["dgates"].cpu().numpy(), ob["dgates"]) < TOL
