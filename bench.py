@@ -214,6 +214,19 @@ def run_ours(args, cfg):
     sync_all()
     if L.error_flag():
         raise RuntimeError("cross-GPU flag wait timed out during warm-up")
+    run_step = step
+    launch_count_reset()
+    step()
+    per_step_launches = launch_count()
+    sync_all()
+    if not args.no_graph:
+        # the whole fwd+bwd step (router, maps, GEMMs, NVLink barriers) as one CUDA graph
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        sync_all()
+        run_step = graph.replay
 
     # ---- device-timed region (inputs resident in HBM) ----
     clocks = ClockSampler(local)
@@ -223,10 +236,10 @@ def run_ours(args, cfg):
     sync_all()
     ev0.record(stream)
     for _ in range(args.steps):
-        step()
+        run_step()
     ev1.record(stream)
     sync_all()
-    launches = launch_count()
+    launches = launch_count() if args.no_graph else per_step_launches * args.steps
     clk = clocks.stop()
     ms_local = ev0.elapsed_time(ev1) / args.steps
     t = torch.tensor([ms_local], device="cuda")
@@ -248,26 +261,53 @@ def run_ours(args, cfg):
     sync_all()
 
     # ---- end-to-end through the public API with host buffers ----
+    # Every step uploads its own x and dy from pinned host memory and reads
+    # dx back. Copies run on a copy stream, double-buffered, so step i+1's
+    # upload overlaps step i's backward and dx's readback overlaps the
+    # weight-gradient GEMMs (dx_event fires before them).
     x_h = x.cpu().pin_memory()
     dy_h = dy.cpu().pin_memory()
     dx_h = torch.empty(Tr, h, dtype=torch.bfloat16).pin_memory()
-    x_d = torch.empty_like(x)
-    dy_d = torch.empty_like(dy)
+    xb = [torch.empty_like(x) for _ in range(2)]
+    dyb = [torch.empty_like(dy) for _ in range(2)]
+    dxb = [torch.empty_like(dx) for _ in range(2)]
+    cs = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    ev_dx = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
 
-    def e2e_step():
-        x_d.copy_(x_h, non_blocking=True)
-        dy_d.copy_(dy_h, non_blocking=True)
-        L.forward(x_d, y)
-        L.backward(dy_d, dx, dw1, dw2, dwr)
-        dx_h.copy_(dx, non_blocking=True)
+    def e2e_run(nsteps):
+        with torch.cuda.stream(cs):
+            xb[0].copy_(x_h, non_blocking=True)
+            dyb[0].copy_(dy_h, non_blocking=True)
+            ev_in[0].record(cs)
+        for i in range(nsteps):
+            b = i % 2
+            stream.wait_event(ev_in[b])
+            L.forward(xb[b], y)
+            if i + 1 < nsteps:
+                with torch.cuda.stream(cs):
+                    if i >= 1:
+                        cs.wait_event(ev_free[1 - b])
+                    xb[1 - b].copy_(x_h, non_blocking=True)
+                    dyb[1 - b].copy_(dy_h, non_blocking=True)
+                    ev_in[1 - b].record(cs)
+            if i >= 2:
+                stream.wait_event(ev_out[b])   # dx buffer b drained to host
+            L.backward(dyb[b], dxb[b], dw1, dw2, dwr, dx_event=ev_dx[b])
+            ev_free[b].record(stream)
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_dx[b])
+                dx_h.copy_(dxb[b], non_blocking=True)
+                ev_out[b].record(cs)
+        stream.wait_stream(cs)
 
-    for _ in range(2):
-        e2e_step()
+    e2e_run(2)
     sync_all()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
+    e2e_run(args.steps)
     e1.record(stream)
     sync_all()
     te = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
@@ -275,6 +315,10 @@ def run_ours(args, cfg):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te.item())
 
+    rt = L.routing()
+    cnt = rt["per_expert_counts"].cpu().tolist()[rank * el:(rank + 1) * el]
+    routing_info = {"local_rows": int(sum(cnt)), "padded_rows": int(sum((c + 255) // 256 * 256 for c in cnt)),
+                    "max_expert_rows": int(max(cnt)), "min_expert_rows": int(min(cnt))}
     if rank == 0:
         peaks = load_peaks()
         rows = Tr * k * n  # expert rows processed per rank (uniform expectation)
@@ -298,8 +342,11 @@ def run_ours(args, cfg):
                          "step_tflops": total_flops / (ms / 1000.0) / 1e12,
                          "step_frac": total_flops / (ms / 1000.0) / 1e12 / peaks["bf16_sus"]},
             "phases_ms": {kk: round(v, 4) for kk, v in phases.items()},
+            "routing_rank0": routing_info,
             "clocks": clk,
             "gpu_launches": int(launches),
+            "gpu_launches_per_step": int(per_step_launches),
+            "launch_mode": "eager" if args.no_graph else "cuda_graph",
             "e2e": {"value": n * Tr / (e2e_ms / 1000.0), "unit": "tokens/s",
                     "h2d_bytes_per_step": 2 * Tr * h * 2, "d2h_bytes_per_step": Tr * h * 2,
                     "ms_per_step": e2e_ms},
@@ -328,6 +375,7 @@ def main():
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-sample", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]

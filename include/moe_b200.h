@@ -193,6 +193,13 @@ moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx
                               uint16_t* d_dw1, uint16_t* d_dw2, float* d_dwr,
                               moe_stream_t stream);
 
+/* As moe_layer_backward; additionally records `dx_ready_event` (a
+ * cudaEvent_t, may be NULL) on `stream` as soon as dx is final, before the
+ * weight-gradient GEMMs, so a caller can overlap dx's transfer with them. */
+moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx,
+                                 uint16_t* d_dw1, uint16_t* d_dw2, float* d_dwr,
+                                 void* dx_ready_event, moe_stream_t stream);
+
 /* Routing results of the last forward (device pointers owned by the layer):
  * experts/gates [T_global, k], dropped [T_global], row_map_in [rows],
  * per_expert_counts [E], out_expert/out_source_rank [rows], rows (device). */
@@ -223,7 +230,7 @@ int moe_layer_error_flag(moe_layer* L);
 moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b, void* d_d, int32_t groups,
                             const int32_t* d_group_rows, int64_t total_rows, int64_t M, int64_t N,
                             int64_t K, int32_t a_mn_major, int32_t b_mn_major, int32_t k_grouped,
-                            int32_t out_f32, int32_t bn, moe_stream_t stream);
+                            int32_t out_f32, int32_t bn, int32_t cta_pair, moe_stream_t stream);
 
 /* ===================================================================== */
 /* Multi-GPU fabric (NVLink P2P over NVSwitch; one process per GPU)       */

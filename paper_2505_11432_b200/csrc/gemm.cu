@@ -7,48 +7,74 @@
 
 namespace moe {
 
-template <int BN, bool A_MN, bool B_MN, bool KG, int EPI>
+template <int BN, int CG, bool A_MN, bool B_MN, bool KG, int EPI>
 static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                               int grid, cudaStream_t s) {
-    using Cfg = GemmCfg<BN>;
-    auto kern = grouped_gemm_kernel<BN, A_MN, B_MN, KG, EPI>;
+    using Cfg = GemmCfg<BN, CG>;
+    auto kern = grouped_gemm_kernel<BN, CG, A_MN, B_MN, KG, EPI>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           Cfg::SMEM_BYTES));
         attr_set = true;
     }
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(ta, tb, a);
+    if (CG == 1) {
+        kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(ta, tb, a);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(grid & ~1));
+        cfg.blockDim = dim3(Cfg::THREADS);
+        cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
+    }
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;
 }
 
 moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s) {
-    MOE_CHECK_ARG(a.G >= 1 && a.G <= GemmCfg<256>::MAX_GROUPS, "grouped GEMM: 1 <= groups <= 256");
+    MOE_CHECK_ARG(a.G >= 1 && a.G <= 256, "grouped GEMM: 1 <= groups <= 256");
     const int grid = p.grid > 0 ? p.grid : kNumSMs;
-#define MOE_GEMM_CASE(BN, AMN, BMN, KG, EPI)                                               \
-    if (p.bn == BN && p.a_mn == AMN && p.b_mn == BMN && p.k_grouped == KG && p.epi == EPI) \
-        return launch_impl<BN, AMN, BMN, KG, EPI>(p.ta, p.tb, a, grid, s);
-    // forward fc1 (fused SwiGLU) / fc2 (scatter to combine staging)
-    MOE_GEMM_CASE(256, false, false, false, EPI_SWIGLU)
-    MOE_GEMM_CASE(256, false, false, false, EPI_SCATTER)
-    // dgrads: weights read MN-major
-    MOE_GEMM_CASE(256, false, true, false, EPI_SWIGLU_BWD)
-    MOE_GEMM_CASE(256, false, true, false, EPI_SCATTER)
-    // wgrads
-    MOE_GEMM_CASE(256, true, true, true, EPI_STORE_BF16)
-    MOE_GEMM_CASE(256, true, true, true, EPI_STORE_F32)
-    // generic (tests / attention projections)
-    MOE_GEMM_CASE(256, false, false, false, EPI_STORE_BF16)
-    MOE_GEMM_CASE(256, false, false, false, EPI_STORE_F32)
-    MOE_GEMM_CASE(256, false, true, false, EPI_STORE_BF16)
-    MOE_GEMM_CASE(256, false, true, false, EPI_STORE_F32)
-    MOE_GEMM_CASE(128, false, false, false, EPI_STORE_BF16)
-    MOE_GEMM_CASE(128, false, false, false, EPI_STORE_F32)
+#define MOE_GEMM_CASE(BN, CG, AMN, BMN, KG, EPI)                                              \
+    if (p.bn == BN && p.cg == CG && p.a_mn == AMN && p.b_mn == BMN && p.k_grouped == KG &&   \
+        p.epi == EPI)                                                                         \
+        return launch_impl<BN, CG, AMN, BMN, KG, EPI>(p.ta, p.tb, a, grid, s);
+    // layer GEMMs, CTA-pair (cta_group::2) versions
+    MOE_GEMM_CASE(256, 2, false, false, false, EPI_SWIGLU)       // fc1 + SwiGLU
+    MOE_GEMM_CASE(256, 2, false, false, false, EPI_SCATTER)      // fc2 + gather
+    MOE_GEMM_CASE(256, 2, false, true, false, EPI_SWIGLU_BWD)    // fc2 dgrad
+    MOE_GEMM_CASE(256, 2, false, true, false, EPI_SCATTER)       // fc1 dgrad
+    MOE_GEMM_CASE(256, 2, true, true, true, EPI_STORE_BF16)      // wgrads
+    MOE_GEMM_CASE(256, 2, true, true, true, EPI_STORE_F32)
+    MOE_GEMM_CASE(256, 2, false, false, false, EPI_STORE_BF16)   // generic
+    MOE_GEMM_CASE(256, 2, false, false, false, EPI_STORE_F32)
+    MOE_GEMM_CASE(256, 2, false, true, false, EPI_STORE_F32)
+    MOE_GEMM_CASE(256, 2, false, true, false, EPI_STORE_BF16)
+    // single-CTA versions
+    MOE_GEMM_CASE(256, 1, false, false, false, EPI_SWIGLU)
+    MOE_GEMM_CASE(256, 1, false, false, false, EPI_SCATTER)
+    MOE_GEMM_CASE(256, 1, false, true, false, EPI_SWIGLU_BWD)
+    MOE_GEMM_CASE(256, 1, false, true, false, EPI_SCATTER)
+    MOE_GEMM_CASE(256, 1, true, true, true, EPI_STORE_BF16)
+    MOE_GEMM_CASE(256, 1, true, true, true, EPI_STORE_F32)
+    MOE_GEMM_CASE(256, 1, false, false, false, EPI_STORE_BF16)
+    MOE_GEMM_CASE(256, 1, false, false, false, EPI_STORE_F32)
+    MOE_GEMM_CASE(256, 1, false, true, false, EPI_STORE_BF16)
+    MOE_GEMM_CASE(256, 1, false, true, false, EPI_STORE_F32)
+    MOE_GEMM_CASE(128, 1, false, false, false, EPI_STORE_BF16)
+    MOE_GEMM_CASE(128, 1, false, false, false, EPI_STORE_F32)
 #undef MOE_GEMM_CASE
-    return set_error(MOE_ERR_UNSUPPORTED, "grouped GEMM variant not instantiated (bn=%d a_mn=%d b_mn=%d kg=%d epi=%d)",
-                     p.bn, (int)p.a_mn, (int)p.b_mn, (int)p.k_grouped, p.epi);
+    return set_error(MOE_ERR_UNSUPPORTED,
+                     "grouped GEMM variant not instantiated (bn=%d cg=%d a_mn=%d b_mn=%d kg=%d epi=%d)",
+                     p.bn, p.cg, (int)p.a_mn, (int)p.b_mn, (int)p.k_grouped, p.epi);
 }
 
 // Tensor maps for the operand layouts used by the kernel.
@@ -71,14 +97,16 @@ extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b,
                                        int64_t total_rows, int64_t M, int64_t N, int64_t K,
                                        int32_t a_mn_major, int32_t b_mn_major,
                                        int32_t k_grouped, int32_t out_f32, int32_t bn,
-                                       moe_stream_t stream) {
+                                       int32_t cta_pair, moe_stream_t stream) {
     const char* env = getenv("MOE_B_BOX_ROWS");
     const int b_box = env ? atoi(env) : 0;
     MOE_CHECK_ARG(d_a && d_b && d_d && d_group_rows, "null pointer");
     MOE_CHECK_ARG(bn == 128 || bn == 256, "bn must be 128 or 256");
     MOE_CHECK_ARG(N % 64 == 0 && K % 64 == 0 && M % 128 == 0 || !k_grouped, "K-grouped: M%128, N%64, K%64");
+    MOE_CHECK_ARG(cta_pair == 0 || cta_pair == 1, "cta_pair must be 0 or 1");
     GemmPlan p;
     p.bn = bn;
+    p.cg = cta_pair ? 2 : 1;
     p.a_mn = a_mn_major != 0;
     p.b_mn = b_mn_major != 0;
     p.k_grouped = k_grouped != 0;
@@ -97,7 +125,7 @@ extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b,
         MOE_TRY(tmap_kmajor(&p.ta, d_a, total_rows, K, 128));
         if (!b_mn_major) {
             a.b_group_stride = (int)N;
-            a.b_box_rows = b_box > 0 ? b_box : bn;
+            a.b_box_rows = b_box > 0 ? b_box : bn / p.cg;
             MOE_TRY(tmap_kmajor(&p.tb, d_b, (int64_t)groups * N, K, a.b_box_rows));
         } else {
             a.b_group_stride = (int)K;

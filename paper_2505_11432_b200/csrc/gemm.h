@@ -9,6 +9,7 @@ namespace moe {
 struct GemmPlan {
     CUtensorMap ta, tb;
     int bn = 256;
+    int cg = 1;       // 2 = CTA pair (cta_group::2, 256-row tiles)
     bool a_mn = false, b_mn = false, k_grouped = false;
     int epi = EPI_STORE_BF16;
     int grid = 0;  // 0 = one CTA per SM

@@ -7,18 +7,23 @@
 // Two grouping modes:
 //   M-grouped (forward fc1/fc2 and both dgrads): groups are expert row
 //     segments of a permuted activation matrix, each padded to a multiple of
-//     128 rows; B_g is expert g's weight.
+//     the tile height; B_g is expert g's weight.
 //   K-grouped (wgrads): D_g = sum over expert g's rows; the rows are the
 //     contraction dimension.
 // Operands are K-major or MN-major (template flags) so dgrad/wgrad read the
 // forward layouts directly (no transposes in HBM).
 //
-// Roles (192 threads, 1 CTA per SM, persistent over a static tile stride):
-//   warp 0 lane 0 : TMA producer (4-stage smem ring, 128B swizzle)
-//   warp 1        : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN)
-//   warps 2..5    : epilogue (tcgen05.ld -> fused op -> global), TMEM
-//                   double-buffered so tile i's epilogue overlaps tile i+1's
-//                   MMA.
+// CG = 1: one CTA per tile, UMMA M=128.
+// CG = 2: a CTA pair (cluster of 2, cta_group::2) per 256-row tile. Each CTA
+//   loads its 128 rows of A and half of B; the leader issues M=256 UMMAs that
+//   read both CTAs' shared memory, halving the per-SM operand traffic.
+//
+// Roles (320 threads, 1 CTA per SM, persistent over a static tile stride):
+//   warp 0 lane 0 : TMA producer (multi-stage smem ring, 128B swizzle)
+//   warp 1        : TMEM allocator; lane 0 of the leader CTA issues tcgen05.mma
+//   warps 2..9    : epilogue, two warps per TMEM lane quarter (each half of the
+//                   columns); TMEM double-buffered so tile i's epilogue
+//                   overlaps tile i+1's MMA.
 #pragma once
 
 #include "common.cuh"
@@ -35,7 +40,7 @@ enum EpiKind : int {
 
 struct GemmArgs {
     int G;                      // number of groups (local experts)
-    const int* group_rows;      // [G] padded rows per group (multiple of 128)
+    const int* group_rows;      // [G] padded rows per group (multiple of the tile height)
     int N;                      // output columns
     int K;                      // M-grouped: contraction length; K-grouped: output rows M
     int b_group_stride;         // B coordinate offset per group (rows or K-rows)
@@ -47,28 +52,31 @@ struct GemmArgs {
     const float* row_gate;      // [padded rows] gate per permuted row (0 for pad rows)
     const uint16_t* aux;        // SWIGLU_BWD: fc1_out (bf16 bits)
     int64_t ld_aux;
-    float* row_part;            // SWIGLU_BWD: dgate partials [padded rows][n_tiles]
+    float* row_part;            // SWIGLU_BWD: dgate partials [padded rows][2*n_tiles]
     const int* row_dst;         // SCATTER: (rank << 27) | slot_row, -1 = skip
     void* const* rank_base;     // SCATTER: per destination rank base pointer
     int gate_rows;              // 1: multiply rows by row_gate in STORE/SCATTER epilogue
-    int b_box_rows;             // K-major B: rows per TMA box (BN or 64)
+    int b_box_rows;             // K-major B: rows per TMA box (0 = whole tile half)
     int interleave_rows;        // K-grouped STORE: map packed a/b-interleaved rows back to
                                 // the reference [a | b] row order (dW1)
 };
 
-template <int BN>
+template <int BN, int CG>
 struct GemmCfg {
-    static constexpr int BM = 128;
+    static constexpr int BM = 128;            // rows per CTA
+    static constexpr int TILE_M = BM * CG;    // rows per (pair) tile
     static constexpr int BK = 64;
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int BN_CTA = BN / CG;    // B rows loaded by each CTA
     static constexpr int A_BYTES = BM * BK * 2;
-    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int B_BYTES = BN_CTA * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int MAX_GROUPS = 256;
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int THREADS = 64 + EPI_WARPS * 32;
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES +
                                       (2 * STAGES + 4) * 8 + 16;
-    static constexpr int THREADS = 192;
 };
 
 // Tile-sequence helper shared by all roles.
@@ -76,10 +84,9 @@ struct TileInfo {
     int g, m, n, kblocks, row0;
 };
 
-template <int BN, bool K_GROUPED>
+template <int TILE_M, bool K_GROUPED>
 __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const int* row_off,
-                                                const GemmArgs& a, int G, int n_tiles) {
-    // binary search the group whose tile range contains t
+                                                const GemmArgs& a, int G) {
     int lo = 0, hi = G - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
@@ -90,28 +97,233 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
     ti.g = lo;
     int li = t - prefix[lo];
     if (!K_GROUPED) {
-        const int mt = a.group_rows[lo] >> 7;
+        const int mt = a.group_rows[lo] / TILE_M;
         ti.n = li / mt;
         ti.m = li - ti.n * mt;
         ti.kblocks = (a.K + 63) / 64;
-        ti.row0 = row_off[lo] + ti.m * 128;
+        ti.row0 = row_off[lo] + ti.m * TILE_M;
     } else {
-        const int mt = a.K >> 7;  // output rows / 128
+        const int mt = a.K / TILE_M;  // output rows / tile
         ti.m = li % mt;
         ti.n = li / mt;
         ti.kblocks = a.group_rows[lo] >> 6;
         ti.row0 = row_off[lo];   // contraction row offset
     }
-    (void)n_tiles;
     return ti;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool K_GROUPED, int EPI>
-__global__ void __launch_bounds__(192, 1)
+// ---- cluster / cta_group::2 helpers ----------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_cta(const void* p, uint32_t rank) {
+    uint32_t out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+    return out;
+}
+__device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map,
+                                                uint32_t leader_bar, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}"
+        ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst_smem) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+                 : "memory");
+}
+
+// ---- epilogue ---------------------------------------------------------------
+// One warp handles 32 rows (its TMEM lane quarter) x `ncols` columns starting
+// at column c_lo of the BN-wide accumulator.
+template <int BN, int EPI, bool K_GROUPED>
+__device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileInfo& ti,
+                                              int64_t orow, uint32_t tbase, int c_lo,
+                                              int half, int n_tiles) {
+    const int n0 = ti.n * BN;
+    constexpr int HALF = BN / 2;
+    if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32 || EPI == EPI_SCATTER) {
+        float gscale = 1.0f;
+        if (args.gate_rows) gscale = args.row_gate[orow];
+        uint16_t* obf = nullptr;
+        float* of32 = nullptr;
+        bool valid = true;
+        if (EPI == EPI_SCATTER) {
+            const int dst = args.row_dst[orow];
+            valid = dst >= 0;
+            if (valid)
+                obf = reinterpret_cast<uint16_t*>(args.rank_base[dst >> 27]) +
+                      (int64_t)(dst & ((1 << 27) - 1)) * args.ldo + n0;
+        } else if (EPI == EPI_STORE_BF16) {
+            obf = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
+        } else {
+            of32 = reinterpret_cast<float*>(args.out) + orow * args.ldo + n0;
+        }
+#pragma unroll 1
+        for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tbase + c0, r);
+            tmem_ld_wait();
+            if (!valid || n0 + c0 >= args.N) continue;
+            if (EPI == EPI_STORE_F32) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    float4 v = make_float4(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale,
+                                           __uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
+                    *reinterpret_cast<float4*>(of32 + c0 + i) = v;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    uint4 v;
+                    v.x = pack_bf16x2(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale);
+                    v.y = pack_bf16x2(__uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
+                    v.z = pack_bf16x2(__uint_as_float(r[i + 4]) * gscale, __uint_as_float(r[i + 5]) * gscale);
+                    v.w = pack_bf16x2(__uint_as_float(r[i + 6]) * gscale, __uint_as_float(r[i + 7]) * gscale);
+                    *reinterpret_cast<uint4*>(obf + c0 + i) = v;
+                }
+            }
+        }
+    } else if constexpr (EPI == EPI_SWIGLU) {
+        // accumulator cols [0,BN/2) = a block, [BN/2,BN) = b block (W1 rows
+        // interleaved per BN/2 block at weight-pack time); this warp takes
+        // a/b pairs [half*BN/4, (half+1)*BN/4)
+        const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
+        uint16_t* o1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
+        uint16_t* o2 = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2 + ti.n * HALF;
+        const int p_lo = half * (HALF / 2);
+#pragma unroll 1
+        for (int c0 = p_lo; c0 < p_lo + HALF / 2; c0 += 32) {
+            uint32_t ra[32], rb[32];
+            tmem_ld32(tbase + c0, ra);
+            tmem_ld32(tbase + HALF + c0, rb);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+                uint32_t pa[4], pb[4], ph[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    pa[q] = pack_bf16x2(__uint_as_float(ra[i + 2 * q]), __uint_as_float(ra[i + 2 * q + 1]));
+                    pb[q] = pack_bf16x2(__uint_as_float(rb[i + 2 * q]), __uint_as_float(rb[i + 2 * q + 1]));
+                    // SwiGLU on the bf16-rounded fc1_out so backward remat is exact
+                    const float2 a2 = unpack_bf16x2(pa[q]);
+                    const float2 b2 = unpack_bf16x2(pb[q]);
+                    ph[q] = pack_bf16x2(a2.x * silu_f(b2.x) * g, a2.y * silu_f(b2.y) * g);
+                }
+                *reinterpret_cast<uint4*>(o1 + c0 + i) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+                *reinterpret_cast<uint4*>(o1 + HALF + c0 + i) = make_uint4(pb[0], pb[1], pb[2], pb[3]);
+                *reinterpret_cast<uint4*>(o2 + c0 + i) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+            }
+        }
+    } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+        // D = d fc2_in for f-columns [n0 + c_lo, +BN/2). fc1_out / dfc1 use the
+        // interleaved [a-block(128) | b-block(128)] layout.
+        const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
+        const uint16_t* f1 = args.aux + orow * args.ld_aux;
+        uint16_t* d1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo;
+        uint16_t* rf = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2;
+        float dg = 0.0f;
+        // software-pipelined fc1_out loads: chunk c+1 in flight while c computes
+        uint4 av[4], bv[4], an[4], bn[4];
+        {
+            const int j = n0 + c_lo;
+            const int ia = (j >> 7) * 256 + (j & 127);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                av[q] = *reinterpret_cast<const uint4*>(f1 + ia + q * 8);
+                bv[q] = *reinterpret_cast<const uint4*>(f1 + ia + 128 + q * 8);
+            }
+        }
+#pragma unroll 1
+        for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
+            const int j = n0 + c0;           // f column
+            const int ia = (j >> 7) * 256 + (j & 127);
+            if (c0 + 32 < c_lo + HALF) {
+                const int jn = j + 32;
+                const int ian = (jn >> 7) * 256 + (jn & 127);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    an[q] = *reinterpret_cast<const uint4*>(f1 + ian + q * 8);
+                    bn[q] = *reinterpret_cast<const uint4*>(f1 + ian + 128 + q * 8);
+                }
+            }
+            uint32_t r[32];
+            tmem_ld32(tbase + c0, r);
+            tmem_ld_wait();
+            uint32_t da[16], db[16], hf[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const uint32_t aw = (&av[q >> 2].x)[q & 3];
+                const uint32_t bw = (&bv[q >> 2].x)[q & 3];
+                const float2 a2 = unpack_bf16x2(aw);
+                const float2 b2 = unpack_bf16x2(bw);
+                const float d0 = __uint_as_float(r[2 * q]), d1v = __uint_as_float(r[2 * q + 1]);
+                const float s0 = 1.0f / (1.0f + __expf(-b2.x)), s1 = 1.0f / (1.0f + __expf(-b2.y));
+                const float si0 = b2.x * s0, si1 = b2.y * s1;
+                dg += d0 * a2.x * si0 + d1v * a2.y * si1;
+                da[q] = pack_bf16x2(d0 * g * si0, d1v * g * si1);
+                db[q] = pack_bf16x2(d0 * g * a2.x * s0 * (1.0f + b2.x * (1.0f - s0)),
+                                    d1v * g * a2.y * s1 * (1.0f + b2.y * (1.0f - s1)));
+                hf[q] = pack_bf16x2(a2.x * si0 * g, a2.y * si1 * g);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                *reinterpret_cast<uint4*>(d1 + ia + q * 8) = make_uint4(da[4 * q], da[4 * q + 1], da[4 * q + 2], da[4 * q + 3]);
+                *reinterpret_cast<uint4*>(d1 + ia + 128 + q * 8) = make_uint4(db[4 * q], db[4 * q + 1], db[4 * q + 2], db[4 * q + 3]);
+                *reinterpret_cast<uint4*>(rf + j + q * 8) = make_uint4(hf[4 * q], hf[4 * q + 1], hf[4 * q + 2], hf[4 * q + 3]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                av[q] = an[q];
+                bv[q] = bn[q];
+            }
+        }
+        if (args.row_part) args.row_part[orow * (2 * n_tiles) + ti.n * 2 + half] = dg;
+    }
+}
+
+template <int BN, int CG, bool A_MN, bool B_MN, bool K_GROUPED, int EPI>
+__global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
-    using Cfg = GemmCfg<BN>;
-    constexpr int BM = Cfg::BM, STAGES = Cfg::STAGES;
+    using Cfg = GemmCfg<BN, CG>;
+    constexpr int BM = Cfg::BM, STAGES = Cfg::STAGES, TILE_M = Cfg::TILE_M;
+    constexpr int BN_CTA = Cfg::BN_CTA;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -127,8 +339,12 @@ __global__ void __launch_bounds__(192, 1)
     const int lane = threadIdx.x & 31;
     const int G = args.G;
     const int n_tiles = (args.N + BN - 1) / BN;
+    const uint32_t cta_rank = CG == 2 ? cluster_ctarank() : 0;
+    const bool leader = cta_rank == 0;
+    const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // tile-stride unit
+    const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-    // --- setup: tile prefix + group row offsets (G <= MAX_GROUPS) -----------
+    // --- setup ---------------------------------------------------------------
     if (threadIdx.x == 0) {
         int acc = 0, racc = 0;
         for (int g = 0; g < G; ++g) {
@@ -136,8 +352,8 @@ __global__ void __launch_bounds__(192, 1)
             s_rowoff[g] = racc;
             const int rows = args.group_rows[g];
             racc += rows;
-            if (!K_GROUPED) acc += (rows >> 7) * n_tiles;
-            else acc += (args.K >> 7) * n_tiles;
+            if (!K_GROUPED) acc += (rows / TILE_M) * n_tiles;
+            else acc += (args.K / TILE_M) * n_tiles;
         }
         prefix[G] = acc;
         s_rowoff[G] = racc;
@@ -151,13 +367,17 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], 4);
+            mbar_init(&tempty_bar[a], Cfg::EPI_WARPS * CG);
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+    if (warp == 1) {
+        if (CG == 2) tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
+        else tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int total_tiles = prefix[G];
@@ -167,55 +387,62 @@ __global__ void __launch_bounds__(192, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                const TileInfo ti = decode_tile<BN, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+            const int arow = (int)cta_rank * BM;       // this CTA's A rows within the tile
+            const int bcol = (int)cta_rank * BN_CTA;   // this CTA's B rows/cols within the tile
+            for (int t = unit; t < total_tiles; t += nunits) {
+                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G);
                 for (int kb = 0; kb < ti.kblocks; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
                     uint8_t* sb = sa + Cfg::A_BYTES;
-                    mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+                    uint64_t* fb = &full_bar[stage];
+                    uint32_t fb_leader = 0;
+                    if (CG == 2) {
+                        fb_leader = map_to_cta(fb, 0);
+                        if (leader) mbar_arrive_expect_tx(fb, CG * Cfg::STAGE_BYTES);
+                    } else {
+                        mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES);
+                    }
+                    auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+                        if (CG == 2) tma_load_2d_2sm(dst, map, fb_leader, c0, c1);
+                        else tma_load_2d(dst, map, fb, c0, c1);
+                    };
                     if (!K_GROUPED) {
-                        // A: permuted activations [rows, K] (K-major) or [K..] n/a
-                        if (!A_MN) {
-                            tma_load_2d(sa, &tmA, &full_bar[stage], kb * 64, ti.row0);
-                        }
+                        load(sa, &tmA, kb * 64, ti.row0 + arow);
                         if (!B_MN) {
-                            const int bbr = args.b_box_rows > 0 ? args.b_box_rows : BN;
-                            for (int j = 0; j < BN; j += bbr)
-                                tma_load_2d(sb + j * 128, &tmB, &full_bar[stage], kb * 64,
-                                            ti.g * args.b_group_stride + ti.n * BN + j);
+                            const int bbr = args.b_box_rows > 0 ? args.b_box_rows : BN_CTA;
+                            for (int j = 0; j < BN_CTA; j += bbr)
+                                load(sb + j * 128, &tmB, kb * 64,
+                                     ti.g * args.b_group_stride + ti.n * BN + bcol + j);
                         } else {
 #pragma unroll
-                            for (int j = 0; j < BN / 64; ++j)
-                                tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage],
-                                            ti.n * BN + j * 64,
-                                            ti.g * args.b_group_stride + kb * 64);
+                            for (int j = 0; j < BN_CTA / 64; ++j)
+                                load(sb + j * 8192, &tmB, ti.n * BN + bcol + j * 64,
+                                     ti.g * args.b_group_stride + kb * 64);
                         }
                     } else {
                         // wgrad: A = [rows, M] MN-major, B = [rows, N] MN-major
 #pragma unroll
                         for (int j = 0; j < BM / 64; ++j)
-                            tma_load_2d(sa + j * 8192, &tmA, &full_bar[stage], ti.m * BM + j * 64,
-                                        ti.row0 + kb * 64);
+                            load(sa + j * 8192, &tmA, ti.m * TILE_M + arow + j * 64, ti.row0 + kb * 64);
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j)
-                            tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], ti.n * BN + j * 64,
-                                        ti.row0 + kb * 64);
+                        for (int j = 0; j < BN_CTA / 64; ++j)
+                            load(sb + j * 8192, &tmB, ti.n * BN + bcol + j * 64, ti.row0 + kb * 64);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        if (lane == 0) {
-            constexpr uint32_t idesc = make_idesc(BM, BN, 1, A_MN, B_MN);
+        // ===================== MMA issuer (leader CTA) =====================
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = make_idesc(TILE_M, BN, 1, A_MN, B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                const TileInfo ti = decode_tile<BN, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+            for (int t = unit; t < total_tiles; t += nunits) {
+                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G);
                 if (ti.kblocks == 0) continue;
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -231,45 +458,51 @@ __global__ void __launch_bounds__(192, 1)
                                                  : make_sdesc(sa + kk * 32, 16, 1024);
                         const uint64_t bd = B_MN ? make_sdesc(sb + kk * 2048, 8192, 1024)
                                                  : make_sdesc(sb + kk * 32, 16, 1024);
-                        umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        if (CG == 2) umma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                     }
-                    umma_commit(&empty_bar[stage]);
+                    if (CG == 2) umma_commit_2sm_mc(&empty_bar[stage]);
+                    else umma_commit(&empty_bar[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                umma_commit(&tfull_bar[acc]);
+                if (CG == 2) umma_commit_2sm_mc(&tfull_bar[acc]);
+                else umma_commit(&tfull_bar[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5) =====================
+        // ===================== epilogue (warps 2..9) =====================
+        const int ew = warp - 2;
         const int quarter = warp & 3;           // TMEM lane quarter this warp may access
-        const int r_in_tile = quarter * 32 + lane;
+        const int half = ew >> 2;               // column half
+        const int r_in_cta = quarter * 32 + lane;
+        const uint32_t tempty_leader = CG == 2 ? map_to_cta(&tempty_bar[0], 0) : 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-            const TileInfo ti = decode_tile<BN, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+        for (int t = unit; t < total_tiles; t += nunits) {
+            const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G);
             const int n0 = ti.n * BN;
-            // output row (global) for this thread
             int64_t orow;
             if (K_GROUPED) {
-                int mi = ti.m * BM + r_in_tile;
+                int mi = ti.m * TILE_M + (int)cta_rank * BM + r_in_cta;
                 if (args.interleave_rows) {
                     const int blk = mi >> 8, w = mi & 255;
                     mi = w < 128 ? blk * 128 + w : (args.K >> 1) + blk * 128 + (w - 128);
                 }
                 orow = (int64_t)ti.g * args.K + mi;
             } else {
-                orow = (int64_t)ti.row0 + r_in_tile;
+                orow = (int64_t)ti.row0 + (int)cta_rank * BM + r_in_cta;
             }
             if (ti.kblocks == 0) {
                 // empty contraction (expert received no rows): D = 0
+                const int c_lo = half * (BN / 2);
                 if (EPI == EPI_STORE_BF16) {
                     uint16_t* o = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
-                    for (int c = 0; c < BN; c += 8)
+                    for (int c = c_lo; c < c_lo + BN / 2; c += 8)
                         if (n0 + c < args.N) *reinterpret_cast<uint4*>(o + c) = make_uint4(0, 0, 0, 0);
                 } else if (EPI == EPI_STORE_F32) {
                     float* o = reinterpret_cast<float*>(args.out) + orow * args.ldo + n0;
-                    for (int c = 0; c < BN; c += 4)
+                    for (int c = c_lo; c < c_lo + BN / 2; c += 4)
                         if (n0 + c < args.N) *reinterpret_cast<float4*>(o + c) = make_float4(0, 0, 0, 0);
                 }
                 continue;
@@ -277,138 +510,24 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-
-            if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32 || EPI == EPI_SCATTER) {
-                float gscale = 1.0f;
-                if (args.gate_rows) gscale = args.row_gate[orow];
-                uint16_t* obf = nullptr;
-                float* of32 = nullptr;
-                bool valid = true;
-                if (EPI == EPI_SCATTER) {
-                    const int dst = args.row_dst[orow];
-                    valid = dst >= 0;
-                    if (valid)
-                        obf = reinterpret_cast<uint16_t*>(args.rank_base[dst >> 27]) +
-                              (int64_t)(dst & ((1 << 27) - 1)) * args.ldo + n0;
-                } else if (EPI == EPI_STORE_BF16) {
-                    obf = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
-                } else {
-                    of32 = reinterpret_cast<float*>(args.out) + orow * args.ldo + n0;
-                }
-#pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
-                    uint32_t r[32];
-                    tmem_ld32(tbase + c0, r);
-                    tmem_ld_wait();
-                    if (!valid || n0 + c0 >= args.N) continue;
-                    if (EPI == EPI_STORE_F32) {
-#pragma unroll
-                        for (int i = 0; i < 32; i += 4) {
-                            float4 v = make_float4(__uint_as_float(r[i]) * gscale,
-                                                   __uint_as_float(r[i + 1]) * gscale,
-                                                   __uint_as_float(r[i + 2]) * gscale,
-                                                   __uint_as_float(r[i + 3]) * gscale);
-                            *reinterpret_cast<float4*>(of32 + c0 + i) = v;
-                        }
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 32; i += 8) {
-                            uint4 v;
-                            v.x = pack_bf16x2(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale);
-                            v.y = pack_bf16x2(__uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
-                            v.z = pack_bf16x2(__uint_as_float(r[i + 4]) * gscale, __uint_as_float(r[i + 5]) * gscale);
-                            v.w = pack_bf16x2(__uint_as_float(r[i + 6]) * gscale, __uint_as_float(r[i + 7]) * gscale);
-                            *reinterpret_cast<uint4*>(obf + c0 + i) = v;
-                        }
-                    }
-                }
-            } else if constexpr (EPI == EPI_SWIGLU) {
-                // accumulator cols [0,BN/2) = a block, [BN/2,BN) = b block
-                // (W1 rows interleaved per BN/2 block at weight-pack time)
-                const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
-                uint16_t* o1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
-                uint16_t* o2 = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2 + ti.n * (BN / 2);
-#pragma unroll 1
-                for (int c0 = 0; c0 < BN / 2; c0 += 32) {
-                    uint32_t ra[32], rb[32];
-                    tmem_ld32(tbase + c0, ra);
-                    tmem_ld32(tbase + BN / 2 + c0, rb);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 32; i += 8) {
-                        uint32_t pa[4], pb[4], ph[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            pa[q] = pack_bf16x2(__uint_as_float(ra[i + 2 * q]), __uint_as_float(ra[i + 2 * q + 1]));
-                            pb[q] = pack_bf16x2(__uint_as_float(rb[i + 2 * q]), __uint_as_float(rb[i + 2 * q + 1]));
-                            // SwiGLU on the bf16-rounded fc1_out so backward remat is exact
-                            const float2 a2 = unpack_bf16x2(pa[q]);
-                            const float2 b2 = unpack_bf16x2(pb[q]);
-                            ph[q] = pack_bf16x2(a2.x * silu_f(b2.x) * g, a2.y * silu_f(b2.y) * g);
-                        }
-                        *reinterpret_cast<uint4*>(o1 + c0 + i) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-                        *reinterpret_cast<uint4*>(o1 + BN / 2 + c0 + i) = make_uint4(pb[0], pb[1], pb[2], pb[3]);
-                        *reinterpret_cast<uint4*>(o2 + c0 + i) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-                    }
-                }
-            } else if constexpr (EPI == EPI_SWIGLU_BWD) {
-                // D = d fc2_in for f-columns [n0, n0+BN). fc1_out / dfc1 are in the
-                // interleaved [a-block(128) | b-block(128)] layout.
-                const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
-                const uint16_t* f1 = args.aux + orow * args.ld_aux;
-                uint16_t* d1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo;
-                uint16_t* rf = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2;
-                float dg = 0.0f;
-#pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
-                    uint32_t r[32];
-                    tmem_ld32(tbase + c0, r);
-                    const int j = n0 + c0;           // f column
-                    const int ia = (j >> 7) * 256 + (j & 127);
-                    uint4 av[4], bv[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        av[q] = *reinterpret_cast<const uint4*>(f1 + ia + q * 8);
-                        bv[q] = *reinterpret_cast<const uint4*>(f1 + ia + 128 + q * 8);
-                    }
-                    tmem_ld_wait();
-                    uint32_t da[16], db[16], hf[16];
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) {
-                        const uint32_t aw = (&av[q >> 2].x)[q & 3];
-                        const uint32_t bw = (&bv[q >> 2].x)[q & 3];
-                        const float2 a2 = unpack_bf16x2(aw);
-                        const float2 b2 = unpack_bf16x2(bw);
-                        const float d0 = __uint_as_float(r[2 * q]), d1v = __uint_as_float(r[2 * q + 1]);
-                        const float s0 = 1.0f / (1.0f + __expf(-b2.x)), s1 = 1.0f / (1.0f + __expf(-b2.y));
-                        const float si0 = b2.x * s0, si1 = b2.y * s1;
-                        dg += d0 * a2.x * si0 + d1v * a2.y * si1;
-                        da[q] = pack_bf16x2(d0 * g * si0, d1v * g * si1);
-                        db[q] = pack_bf16x2(d0 * g * a2.x * s0 * (1.0f + b2.x * (1.0f - s0)),
-                                            d1v * g * a2.y * s1 * (1.0f + b2.y * (1.0f - s1)));
-                        hf[q] = pack_bf16x2(a2.x * si0 * g, a2.y * si1 * g);
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        *reinterpret_cast<uint4*>(d1 + ia + q * 8) = make_uint4(da[4 * q], da[4 * q + 1], da[4 * q + 2], da[4 * q + 3]);
-                        *reinterpret_cast<uint4*>(d1 + ia + 128 + q * 8) = make_uint4(db[4 * q], db[4 * q + 1], db[4 * q + 2], db[4 * q + 3]);
-                        *reinterpret_cast<uint4*>(rf + j + q * 8) = make_uint4(hf[4 * q], hf[4 * q + 1], hf[4 * q + 2], hf[4 * q + 3]);
-                    }
-                }
-                if (args.row_part) args.row_part[orow * n_tiles + ti.n] = dg;
-            }
+            epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, half * (BN / 2), half, n_tiles);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
+                else mbar_arrive(&tempty_bar[acc]);
+            }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
 
     __syncwarp();
     __syncthreads();
+    if (CG == 2) cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+        if (CG == 2) tmem_dealloc_2sm<Cfg::TMEM_COLS>(tmem_base);
+        else tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
     }
 }
 

@@ -22,16 +22,18 @@ namespace moe {
 
 namespace {
 size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+constexpr int kCG = 2;          // CTA-pair GEMMs
+constexpr int kPad = 128 * kCG;  // expert row segments padded to the tile height
 }  // namespace
 
 enum Phase {
     PH_ROUTE, PH_PERMUTE, PH_DISPATCH, PH_FC1, PH_FC2, PH_COMBINE, PH_FWD_END,
-    PH_DISPATCH_DY, PH_FC2_DGRAD, PH_FC2_WGRAD, PH_FC1_DGRAD, PH_FC1_WGRAD, PH_DGATE,
-    PH_COMBINE_DX, PH_ROUTER_WGRAD, PH_END, PH_COUNT
+    PH_DISPATCH_DY, PH_FC2_DGRAD, PH_FC1_DGRAD, PH_DGATE, PH_COMBINE_DX, PH_FC2_WGRAD,
+    PH_FC1_WGRAD, PH_ROUTER_WGRAD, PH_END, PH_COUNT
 };
 static const char* kPhaseNames[PH_COUNT] = {
     "route", "permute", "dispatch", "fc1", "fc2", "combine", "fwd_end", "dispatch_dy", "fc2_dgrad",
-    "fc2_wgrad", "fc1_dgrad", "fc1_wgrad", "dgate", "combine_dx", "router_wgrad", "end"};
+    "fc1_dgrad", "dgate", "combine_dx", "fc2_wgrad", "fc1_wgrad", "router_wgrad", "end"};
 
 }  // namespace moe
 
@@ -69,7 +71,7 @@ struct moe_layer {
     float** t_dgate = nullptr;
     uint32_t** t_flags = nullptr;
     int* err = nullptr;
-    uint32_t epoch = 0;
+    uint32_t* epoch_dev = nullptr;
     bool router_attr = false;
     bool weights_set = false, routing_set = false, fwd_done = false, ipc_ready = false;
     // GEMM plans (tensor maps fixed at create / set_weights)
@@ -139,12 +141,12 @@ moe_status build_plans(moe_layer* L) {
     L->p_fc1 = GemmPlan{};
     L->p_fc1.epi = EPI_SWIGLU;
     MOE_TRY(tmap_kmajor(&L->p_fc1.ta, L->x_perm, Mp, h, 128));
-    MOE_TRY(tmap_kmajor(&L->p_fc1.tb, L->w1p, el * 2 * f, h, 256));
+    MOE_TRY(tmap_kmajor(&L->p_fc1.tb, L->w1p, el * 2 * f, h, 256 / kCG));
     // forward fc2: A = fc2_in [Mp, f], B = w2 [el*h, f] (K-major)
     L->p_fc2 = GemmPlan{};
     L->p_fc2.epi = EPI_SCATTER;
     MOE_TRY(tmap_kmajor(&L->p_fc2.ta, L->fc2_in, Mp, f, 128));
-    MOE_TRY(tmap_kmajor(&L->p_fc2.tb, L->w2, el * h, f, 256));
+    MOE_TRY(tmap_kmajor(&L->p_fc2.tb, L->w2, el * h, f, 256 / kCG));
     // fc2 dgrad: A = dy_perm [Mp, h], B(n=f, k=h) = w2[e][k][n] (MN-major)
     L->p_fc2_dgrad = GemmPlan{};
     L->p_fc2_dgrad.epi = EPI_SWIGLU_BWD;
@@ -169,14 +171,17 @@ moe_status build_plans(moe_layer* L) {
     L->p_fc1_wgrad.a_mn = L->p_fc1_wgrad.b_mn = L->p_fc1_wgrad.k_grouped = true;
     MOE_TRY(tmap_mnmajor(&L->p_fc1_wgrad.ta, L->dfc1, Mp, 2 * f));
     MOE_TRY(tmap_mnmajor(&L->p_fc1_wgrad.tb, L->x_perm, Mp, h));
+    for (GemmPlan* p : {&L->p_fc1, &L->p_fc2, &L->p_fc2_dgrad, &L->p_fc2_wgrad, &L->p_fc1_dgrad,
+                        &L->p_fc1_wgrad})
+        p->cg = kCG;
     return MOE_OK;
 }
 
-moe_status barrier(moe_layer* L, int slot, cudaStream_t s) {
+moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
     if (L->n == 1) return MOE_OK;
     if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
-    flag_barrier_kernel<<<1, 64, 0, s>>>(L->t_flags, slot, (int)L->n, (int)L->rank, L->epoch,
-                                        20ull * 1000 * 1000 * 1000, L->err);
+    flag_barrier_kernel<<<1, 64, 0, s>>>(L->t_flags, slot, (int)L->n, (int)L->rank, L->epoch_dev,
+                                        bump, 20ull * 1000 * 1000 * 1000, L->err);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;
@@ -212,7 +217,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     L->k = c.top_k;
     L->el = L->E / L->n;
     L->first = L->rank * L->el;
-    L->Mp = L->T * L->k + L->el * 128;
+    L->Mp = L->T * L->k + L->el * kPad;
     MOE_CHECK_ARG(L->T * L->k < (1ll << 27), "T*k must be < 2^27");
     cudaGetDevice(&L->dev);
 
@@ -260,7 +265,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->fc2_in, Mp * f));
     TRY_ALLOC(dalloc(&L->dy_perm, Mp * h));
     TRY_ALLOC(dalloc(&L->dfc1, Mp * 2 * f));
-    TRY_ALLOC(dalloc(&L->dgate_part, Mp * (f / 256)));
+    TRY_ALLOC(dalloc(&L->dgate_part, Mp * (f / 256) * 2));
     TRY_ALLOC(dalloc(&L->dlogits, L->Tr * L->E));
     TRY_ALLOC(dalloc(&L->rw_part, ((L->Tr + kRwChunk - 1) / kRwChunk) * L->E * h));
     TRY_ALLOC(dalloc(&L->t_x, L->n));
@@ -273,6 +278,8 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->t_flags, L->n));
     TRY_ALLOC(dalloc(&L->err, 1));
     cudaMemset(L->err, 0, sizeof(int));
+    TRY_ALLOC(dalloc(&L->epoch_dev, 1));
+    cudaMemset(L->epoch_dev, 0, sizeof(uint32_t));
     // zero the permuted buffers once so never-written rows are finite
     cudaMemset(L->x_perm, 0, Mp * h * 2);
     cudaMemset(L->dy_perm, 0, Mp * h * 2);
@@ -304,7 +311,7 @@ void moe_layer_destroy(moe_layer* L) {
                     L->expert_off, L->rows, L->gpad_rows, L->gpad_off, L->pad_tok, L->row_dst,
                     L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
                     L->dgate_part, L->dlogits, L->rw_part, L->t_x, L->t_dy, L->t_stage, L->t_dstage, L->t_ex,
-                    L->t_gt, L->t_dgate, L->t_flags, L->err};
+                    L->t_gt, L->t_dgate, L->t_flags, L->err, L->epoch_dev};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
@@ -368,11 +375,10 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         }
     }
     // routing metadata all-gather over NVLink
-    ++L->epoch;
     publish_meta_kernel<<<std::min<int64_t>((Tr * k + 255) / 256, 64), 256, 0, s>>>(
         L->ex_loc, L->gt_loc, (int)(Tr * k), (int)(L->rank * Tr * k), L->t_ex, L->t_gt, (int)L->n);
     count_launch();
-    MOE_TRY(barrier(L, 0, s));
+    MOE_TRY(barrier(L, 0, s, 1));
     L->mark(PH_PERMUTE, s);
     // K2: capacity drop (replicated on every rank over the global order) + permutation
     if (L->cfg.capacity_factor > 0.0)
@@ -382,7 +388,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         MOE_CUDA_TRY(cudaMemsetAsync(L->dropped, 0, L->T, s));
     MOE_TRY(launch_permute(L->ex_all(), L->src, L->dropped, L->T, L->E, k, L->n, L->rank, L->n,
                            L->row_map_in, L->counts, L->out_expert, L->out_src, L->expert_off,
-                           L->rows, L->perm_ws, L->gpad_rows, L->gpad_off, L->pad_tok, 128, s));
+                           L->rows, L->perm_ws, L->gpad_rows, L->gpad_off, L->pad_tok, kPad, s));
     row_info_kernel<<<(unsigned)el, 256, 0, s>>>(L->gpad_off, L->gpad_rows, L->expert_off,
                                                  L->pad_tok, L->gt_all(), (int)k, (int)Tr,
                                                  L->row_gate, L->row_dst);
@@ -426,7 +432,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         a.gate_rows = gate_before ? 0 : 1;
         MOE_TRY(gemm_launch(L->p_fc2, a, s));
     }
-    MOE_TRY(barrier(L, 1, s));
+    MOE_TRY(barrier(L, 1, s, 0));
     // combine: fixed-order fp32 reduce over the k slots
     L->mark(PH_COMBINE, s);
     combine_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->stage_sym(), L->dropped + L->rank * Tr,
@@ -439,8 +445,9 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     return MOE_OK;
 }
 
-moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx, uint16_t* d_dw1,
-                              uint16_t* d_dw2, float* d_dwr, moe_stream_t stream) {
+moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx,
+                                 uint16_t* d_dw1, uint16_t* d_dw2, float* d_dwr,
+                                 void* dx_ready_event, moe_stream_t stream) {
     MOE_CHECK_ARG(L && d_dy && d_dx, "null argument");
     MOE_CHECK_ARG(L->fwd_done, "backward needs a preceding forward");
     if (L->cfg.gate_order != MOE_GATE_BEFORE_FC2)
@@ -452,8 +459,7 @@ moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx
         MOE_CUDA_TRY(cudaMemcpyAsync(L->dy_sym(), d_dy, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
     // dgates of dropped (token, slot)s are never written by an expert rank
     MOE_CUDA_TRY(cudaMemsetAsync(L->dgate_sym(), 0, Tr * k * 4, s));
-    ++L->epoch;
-    MOE_TRY(barrier(L, 2, s));
+    MOE_TRY(barrier(L, 2, s, 1));
     // AG(dy) + scatter into permuted order
     dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
                                                      (int)Tr, (int)h, L->t_dy, L->dy_perm);
@@ -477,17 +483,7 @@ moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx
         a.row_part = L->dgate_part;
         MOE_TRY(gemm_launch(L->p_fc2_dgrad, a, s));
     }
-    L->mark(PH_FC2_WGRAD, s);
-    if (d_dw2) {
-        GemmArgs a{};
-        a.G = (int)el;
-        a.group_rows = L->gpad_rows;
-        a.N = (int)f;
-        a.K = (int)h;  // output rows per expert
-        a.out = d_dw2;
-        a.ldo = f;
-        MOE_TRY(gemm_launch(L->p_fc2_wgrad, a, s));
-    }
+    // fc1 dgrad + gather of dx rows to the owning rank (GEMM + RS)
     L->mark(PH_FC1_DGRAD, s);
     {
         GemmArgs a{};
@@ -501,6 +497,33 @@ moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx
         a.rank_base = L->t_dstage;
         MOE_TRY(gemm_launch(L->p_fc1_dgrad, a, s));
     }
+    L->mark(PH_DGATE, s);
+    dgate_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgate_part, (int)(f / 256) * 2, L->row_dst,
+                                                L->gpad_off + el, L->t_dgate);
+    count_launch();
+    MOE_TRY(barrier(L, 3, s, 0));
+    L->mark(PH_COMBINE_DX, s);
+    const bool router = L->cfg.route_mode == 0;
+    combine_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(
+        L->dstage_sym(), L->dropped + L->rank * Tr, (int)Tr, (int)k, (int)h, d_dx,
+        router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
+        router ? L->dgate_sym() : nullptr, router ? L->wr : nullptr,
+        router ? L->dlogits : nullptr, (int)L->E);
+    count_launch();
+    // dx is final here: callers may start its device->host copy while the
+    // weight gradients below run (wgrad hidden under the dx transfer)
+    if (dx_ready_event) MOE_CUDA_TRY(cudaEventRecord((cudaEvent_t)dx_ready_event, s));
+    L->mark(PH_FC2_WGRAD, s);
+    if (d_dw2) {
+        GemmArgs a{};
+        a.G = (int)el;
+        a.group_rows = L->gpad_rows;
+        a.N = (int)f;
+        a.K = (int)h;  // output rows per expert
+        a.out = d_dw2;
+        a.ldo = f;
+        MOE_TRY(gemm_launch(L->p_fc2_wgrad, a, s));
+    }
     L->mark(PH_FC1_WGRAD, s);
     if (d_dw1) {
         GemmArgs a{};
@@ -513,19 +536,6 @@ moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx
         a.interleave_rows = 1;
         MOE_TRY(gemm_launch(L->p_fc1_wgrad, a, s));
     }
-    L->mark(PH_DGATE, s);
-    dgate_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgate_part, (int)(f / 256), L->row_dst,
-                                                L->gpad_off + el, L->t_dgate);
-    count_launch();
-    MOE_TRY(barrier(L, 3, s));
-    L->mark(PH_COMBINE_DX, s);
-    const bool router = L->cfg.route_mode == 0;
-    combine_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(
-        L->dstage_sym(), L->dropped + L->rank * Tr, (int)Tr, (int)k, (int)h, d_dx,
-        router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
-        router ? L->dgate_sym() : nullptr, router ? L->wr : nullptr,
-        router ? L->dlogits : nullptr, (int)L->E);
-    count_launch();
     L->mark(PH_ROUTER_WGRAD, s);
     if (d_dwr) {
         if (router) {
@@ -546,6 +556,11 @@ moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx
     MOE_CUDA_TRY(cudaGetLastError());
     L->mark(PH_END, s);
     return MOE_OK;
+}
+
+moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx, uint16_t* d_dw1,
+                              uint16_t* d_dw2, float* d_dwr, moe_stream_t stream) {
+    return moe_layer_backward_ex(L, d_dy, d_dx, d_dw1, d_dw2, d_dwr, nullptr, stream);
 }
 
 moe_status moe_layer_routing(moe_layer* L, moe_layer_routing_view* v) {

@@ -234,9 +234,21 @@ __global__ void publish_meta_kernel(const int32_t* __restrict__ ex, const float*
 
 // Device-side barrier over NVLink: rank r stores `epoch` into slot[r] of
 // every peer's flag array (release, system scope), then waits until its own
-// array holds >= epoch for all peers. Bounded spin -> *err = 1 on timeout.
+// array holds >= epoch for all peers. The epoch lives in device memory and
+// is bumped on the device (bump = 1 at the first barrier of a pass), so the
+// whole layer can be captured once in a CUDA graph and replayed. Bounded
+// spin -> *err = 1 on timeout instead of a hang.
 __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot, int n, int rank,
-                                    uint32_t epoch, unsigned long long timeout_ns, int* err) {
+                                    uint32_t* epoch_dev, int bump, unsigned long long timeout_ns,
+                                    int* err) {
+    __shared__ uint32_t s_epoch;
+    if (threadIdx.x == 0) {
+        uint32_t e = *epoch_dev;
+        if (bump) *epoch_dev = ++e;
+        s_epoch = e;
+    }
+    __syncthreads();
+    const uint32_t epoch = s_epoch;
     const int i = threadIdx.x;
     if (i < n) {
         __threadfence_system();

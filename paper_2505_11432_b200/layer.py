@@ -103,7 +103,9 @@ class MoELayer:
         return y
 
     def backward(self, dy: torch.Tensor, dx=None, dw1=None, dw2=None, dwr=None, want_weight_grads=True,
-                 stream=None):
+                 dx_event: "torch.cuda.Event | None" = None, stream=None):
+        """dx first (fc2 dgrad + SwiGLU bwd, fc1 dgrad + gather, combine), then
+        the weight gradients; `dx_event` is recorded as soon as dx is final."""
         require_cuda(dy)
         dy = dy.contiguous()
         if dx is None:
@@ -115,8 +117,9 @@ class MoELayer:
                 dw2 = torch.empty(self.el, self.h, self.f, dtype=torch.bfloat16, device="cuda")
             if dwr is None:
                 dwr = torch.empty(self.E, self.h, dtype=torch.float32, device="cuda")
-        check(lib().moe_layer_backward(self._h, ptr(dy), ptr(dx), ptr(dw1), ptr(dw2), ptr(dwr),
-                                       stream_ptr(stream)))
+        ev = C.c_void_p(dx_event.cuda_event) if dx_event is not None else C.c_void_p(None)
+        check(lib().moe_layer_backward_ex(self._h, ptr(dy), ptr(dx), ptr(dw1), ptr(dw2), ptr(dwr), ev,
+                                          stream_ptr(stream)))
         return dx, dw1, dw2, dwr
 
     def routing(self):

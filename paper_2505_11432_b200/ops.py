@@ -10,10 +10,10 @@ from ._lib import DomainError, check, i64, lib, ptr, require_cuda, stream_ptr
 
 def grouped_gemm(a: torch.Tensor, b: torch.Tensor, group_rows: torch.Tensor, *, N: int, K: int,
                  M: int = 0, a_mn_major=False, b_mn_major=False, k_grouped=False,
-                 out_dtype=torch.bfloat16, bn=256, out=None, stream=None) -> torch.Tensor:
+                 out_dtype=torch.bfloat16, bn=256, cta_pair=False, out=None, stream=None) -> torch.Tensor:
     """M-grouped: a [rows, K] (K-major), b [G*N, K] (K-major) or [G*K, N]
     (MN-major) -> out [rows, N]; group g owns group_rows[g] rows (multiple
-    of 128). K-grouped: a [rows, M], b [rows, N] (both MN-major) ->
+    of 128, or of 256 with cta_pair). K-grouped: a [rows, M], b [rows, N] (both MN-major) ->
     out [G*M, N], out_g = a_g^T b_g."""
     require_cuda(a, b, group_rows)
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
@@ -25,7 +25,8 @@ def grouped_gemm(a: torch.Tensor, b: torch.Tensor, group_rows: torch.Tensor, *, 
         out = torch.empty(shape, dtype=out_dtype, device=a.device)
     check(lib().moe_grouped_gemm(ptr(a), ptr(b), ptr(out), G, ptr(group_rows), i64(rows), i64(M),
                                  i64(N), i64(K), int(a_mn_major), int(b_mn_major), int(k_grouped),
-                                 int(out.dtype == torch.float32), int(bn), stream_ptr(stream)))
+                                 int(out.dtype == torch.float32), int(bn), int(bool(cta_pair)),
+                                 stream_ptr(stream)))
     return out
 
 

@@ -15,8 +15,13 @@ def _rel(a, b):
     ([128], 256, 64, 256), ([128], 256, 512, 256), ([256, 128, 384], 512, 1024, 256),
     ([128, 0, 256], 256, 256, 256), ([128] * 4, 384, 320, 128), ([512, 640], 1024, 4096, 256),
 ])
-def test_m_grouped_kmajor(rows_per_group, N, K, bn):
+@pytest.mark.parametrize("cta_pair", [False, True])
+def test_m_grouped_kmajor(rows_per_group, N, K, bn, cta_pair):
     from paper_2505_11432_b200 import ops
+    if cta_pair:
+        if bn != 256:
+            pytest.skip("CTA pairs use 256-wide tiles")
+        rows_per_group = [r * 2 for r in rows_per_group]   # multiples of 256
     torch.manual_seed(1)
     G = len(rows_per_group)
     rows = sum(rows_per_group)
@@ -24,7 +29,7 @@ def test_m_grouped_kmajor(rows_per_group, N, K, bn):
     b = torch.randn(G * N, K, device="cuda").bfloat16()
     gr = torch.tensor(rows_per_group, dtype=torch.int32, device="cuda")
     for dt in (torch.float32, torch.bfloat16):
-        out = ops.grouped_gemm(a, b, gr, N=N, K=K, out_dtype=dt, bn=bn)
+        out = ops.grouped_gemm(a, b, gr, N=N, K=K, out_dtype=dt, bn=bn, cta_pair=cta_pair)
         off = 0
         for g, r in enumerate(rows_per_group):
             if r == 0:
@@ -35,15 +40,18 @@ def test_m_grouped_kmajor(rows_per_group, N, K, bn):
 
 
 @pytest.mark.parametrize("rows_per_group,N,K", [([128], 256, 64), ([256, 128], 512, 768)])
-def test_m_grouped_b_mnmajor(rows_per_group, N, K):
+@pytest.mark.parametrize("cta_pair", [False, True])
+def test_m_grouped_b_mnmajor(rows_per_group, N, K, cta_pair):
     from paper_2505_11432_b200 import ops
+    if cta_pair:
+        rows_per_group = [r * 2 for r in rows_per_group]
     torch.manual_seed(2)
     G = len(rows_per_group)
     rows = sum(rows_per_group)
     a = torch.randn(rows, K, device="cuda").bfloat16()
     b = torch.randn(G * K, N, device="cuda").bfloat16()   # per group [K, N]
     gr = torch.tensor(rows_per_group, dtype=torch.int32, device="cuda")
-    out = ops.grouped_gemm(a, b, gr, N=N, K=K, b_mn_major=True, out_dtype=torch.float32)
+    out = ops.grouped_gemm(a, b, gr, N=N, K=K, b_mn_major=True, out_dtype=torch.float32, cta_pair=cta_pair)
     off = 0
     for g, r in enumerate(rows_per_group):
         ref = a[off:off + r].float() @ b[g * K:(g + 1) * K].float()
@@ -51,8 +59,9 @@ def test_m_grouped_b_mnmajor(rows_per_group, N, K):
         off += r
 
 
-@pytest.mark.parametrize("rows_per_group,M,N", [([128], 128, 256), ([256, 0, 384], 256, 512)])
-def test_k_grouped_wgrad(rows_per_group, M, N):
+@pytest.mark.parametrize("rows_per_group,M,N", [([128], 256, 256), ([256, 0, 384], 512, 512)])
+@pytest.mark.parametrize("cta_pair", [False, True])
+def test_k_grouped_wgrad(rows_per_group, M, N, cta_pair):
     from paper_2505_11432_b200 import ops
     torch.manual_seed(3)
     G = len(rows_per_group)
@@ -61,7 +70,7 @@ def test_k_grouped_wgrad(rows_per_group, M, N):
     b = torch.randn(rows, N, device="cuda").bfloat16()
     gr = torch.tensor(rows_per_group, dtype=torch.int32, device="cuda")
     out = ops.grouped_gemm(a, b, gr, N=N, K=0, M=M, a_mn_major=True, b_mn_major=True,
-                           k_grouped=True, out_dtype=torch.float32)
+                           k_grouped=True, out_dtype=torch.float32, cta_pair=cta_pair)
     off = 0
     for g, r in enumerate(rows_per_group):
         ref = a[off:off + r].float().T @ b[off:off + r].float()
