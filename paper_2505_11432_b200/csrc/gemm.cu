@@ -7,11 +7,12 @@
 
 namespace moe {
 
-template <int BN, int CG, bool A_MN, bool B_MN, bool KG, int EPI>
+template <int BN, int CG, bool A_MN, bool B_MN, bool KG, int EPI, bool DISP = false>
 static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                               int grid, cudaStream_t s) {
     using Cfg = GemmCfg<BN, CG>;
-    auto kern = grouped_gemm_kernel<BN, CG, A_MN, B_MN, KG, EPI>;
+    auto kern = grouped_gemm_kernel<BN, CG, A_MN, B_MN, KG, EPI, DISP>;
+    constexpr int kThreads = Cfg::THREADS + (DISP ? 32 * Cfg::COMM_WARPS : 0);
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -19,11 +20,11 @@ static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, cons
         attr_set = true;
     }
     if (CG == 1) {
-        kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(ta, tb, a);
+        kern<<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(ta, tb, a);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(grid & ~1));
-        cfg.blockDim = dim3(Cfg::THREADS);
+        cfg.blockDim = dim3(kThreads);
         cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -45,8 +46,17 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s) {
     const int grid = p.grid > 0 ? p.grid : kNumSMs;
 #define MOE_GEMM_CASE(BN, CG, AMN, BMN, KG, EPI)                                              \
     if (p.bn == BN && p.cg == CG && p.a_mn == AMN && p.b_mn == BMN && p.k_grouped == KG &&   \
-        p.epi == EPI)                                                                         \
+        p.epi == EPI && !p.dispatch)                                                          \
         return launch_impl<BN, CG, AMN, BMN, KG, EPI>(p.ta, p.tb, a, grid, s);
+#define MOE_GEMM_CASE_DISP(BN, CG, AMN, BMN, KG, EPI)                                         \
+    if (p.bn == BN && p.cg == CG && p.a_mn == AMN && p.b_mn == BMN && p.k_grouped == KG &&   \
+        p.epi == EPI && p.dispatch)                                                           \
+        return launch_impl<BN, CG, AMN, BMN, KG, EPI, true>(p.ta, p.tb, a, grid, s);
+    // fused AG + scatter + GroupedGEMM (fc1 forward, fc2 dgrad)
+    MOE_GEMM_CASE_DISP(256, 2, false, false, false, EPI_SWIGLU)
+    MOE_GEMM_CASE_DISP(256, 2, false, true, false, EPI_SWIGLU_BWD)
+    MOE_GEMM_CASE_DISP(256, 1, false, false, false, EPI_SWIGLU)
+    MOE_GEMM_CASE_DISP(256, 1, false, true, false, EPI_SWIGLU_BWD)
     // layer GEMMs, CTA-pair (cta_group::2) versions
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_SWIGLU)       // fc1 + SwiGLU
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_SCATTER)      // fc2 + gather
@@ -72,6 +82,7 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s) {
     MOE_GEMM_CASE(128, 1, false, false, false, EPI_STORE_BF16)
     MOE_GEMM_CASE(128, 1, false, false, false, EPI_STORE_F32)
 #undef MOE_GEMM_CASE
+#undef MOE_GEMM_CASE_DISP
     return set_error(MOE_ERR_UNSUPPORTED,
                      "grouped GEMM variant not instantiated (bn=%d cg=%d a_mn=%d b_mn=%d kg=%d epi=%d)",
                      p.bn, p.cg, (int)p.a_mn, (int)p.b_mn, (int)p.k_grouped, p.epi);

@@ -12,6 +12,7 @@ struct GemmPlan {
     int cg = 1;       // 2 = CTA pair (cta_group::2, 256-row tiles)
     bool a_mn = false, b_mn = false, k_grouped = false;
     int epi = EPI_STORE_BF16;
+    bool dispatch = false;  // fused AG + scatter of the A operand
     int grid = 0;  // 0 = one CTA per SM
 };
 

@@ -59,6 +59,14 @@ struct GemmArgs {
     int b_box_rows;             // K-major B: rows per TMA box (0 = whole tile half)
     int interleave_rows;        // K-grouped STORE: map packed a/b-interleaved rows back to
                                 // the reference [a | b] row order (dW1)
+    // fused dispatch (AG + local scatter into the A operand, DISPATCH = true)
+    const int32_t* pad_row_tok;         // [padded rows] t*k+slot, -1 = pad row
+    const int32_t* nrows_pad;           // device: total padded rows
+    const uint16_t* const* src_bufs;    // per source rank: token rows [T_r, K]
+    uint16_t* a_dst;                    // A operand base (permuted rows) written in-kernel
+    uint32_t* ready;                    // [padded rows / TILE_M] rows landed per tile block
+    int topk, tokens_per_rank;
+    int* err;                           // set to 2 on a dispatch wait timeout
 };
 
 template <int BN, int CG>
@@ -74,6 +82,7 @@ struct GemmCfg {
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int MAX_GROUPS = 256;
     static constexpr int EPI_WARPS = 8;
+    static constexpr int COMM_WARPS = 2;   // only launched for the fused-dispatch variant
     static constexpr int THREADS = 64 + EPI_WARPS * 32;
     static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES +
                                       (2 * STAGES + 4) * 8 + 16;
@@ -86,7 +95,7 @@ struct TileInfo {
 
 template <int TILE_M, bool K_GROUPED>
 __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const int* row_off,
-                                                const GemmArgs& a, int G) {
+                                                const GemmArgs& a, int G, int n_tiles) {
     int lo = 0, hi = G - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
@@ -103,9 +112,10 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
         ti.kblocks = (a.K + 63) / 64;
         ti.row0 = row_off[lo] + ti.m * TILE_M;
     } else {
-        const int mt = a.K / TILE_M;  // output rows / tile
-        ti.m = li % mt;
-        ti.n = li / mt;
+        // n fastest: a wave of tiles shares a few A panels and streams all
+        // of B's (small) contraction panel from L2
+        ti.n = li % n_tiles;
+        ti.m = li / n_tiles;
         ti.kblocks = a.group_rows[lo] >> 6;
         ti.row0 = row_off[lo];   // contraction row offset
     }
@@ -317,8 +327,45 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
     }
 }
 
-template <int BN, int CG, bool A_MN, bool B_MN, bool K_GROUPED, int EPI>
-__global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
+// Fused dispatch: COMM_WARPS extra warps per CTA pull the permuted A rows
+// (from the owning rank's buffer; peers over NVLink) in padded-row order,
+// and publish per-tile-block arrival counts; the TMA producer waits for its
+// tile block's count before loading (tile-level AG -> GEMM overlap, the
+// reference's AG+scatter+GroupedGEMM fused pair, schedule.cpp:225-242).
+template <int TILE_M>
+__device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid, int nw, int lane) {
+    const int total = *a.nrows_pad;
+    const int nvec = K / 8;
+    for (int pp = wid; pp < total; pp += nw) {
+        const int i = a.pad_row_tok[pp];
+        uint4* d = reinterpret_cast<uint4*>(a.a_dst + (int64_t)pp * K);
+        if (i < 0) {
+            for (int v = lane; v < nvec; v += 32) d[v] = make_uint4(0, 0, 0, 0);
+        } else {
+            const int t = i / a.topk;
+            const int src = t / a.tokens_per_rank;
+            const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs[src] +
+                                                             (int64_t)(t - src * a.tokens_per_rank) * K);
+            int v = lane;
+            for (; v + 224 < nvec; v += 256) {
+                uint4 r[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) r[q] = sp[v + 32 * q];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) d[v + 32 * q] = r[q];
+            }
+            for (; v < nvec; v += 32) d[v] = sp[v];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async_global();
+            red_release_gpu_add(&a.ready[pp / TILE_M], 1u);
+        }
+    }
+}
+
+template <int BN, int CG, bool A_MN, bool B_MN, bool K_GROUPED, int EPI, bool DISPATCH = false>
+__global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * GemmCfg<BN, CG>::COMM_WARPS : 0), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
     using Cfg = GemmCfg<BN, CG>;
@@ -390,7 +437,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
             const int arow = (int)cta_rank * BM;       // this CTA's A rows within the tile
             const int bcol = (int)cta_rank * BN_CTA;   // this CTA's B rows/cols within the tile
             for (int t = unit; t < total_tiles; t += nunits) {
-                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G);
+                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
                 for (int kb = 0; kb < ti.kblocks; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
@@ -408,6 +455,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
                         else tma_load_2d(dst, map, fb, c0, c1);
                     };
                     if (!K_GROUPED) {
+                        if (DISPATCH && kb == 0) {
+                            // wait until this tile block's permuted rows have landed
+                            const uint32_t* rdy = &args.ready[ti.row0 / TILE_M];
+                            const uint64_t t0 = globaltimer();
+                            while (ld_acquire_gpu(rdy) < (uint32_t)TILE_M) {
+                                if (globaltimer() - t0 > 4000000000ull) {
+                                    atomicExch(args.err, 2);
+                                    break;
+                                }
+                            }
+                            fence_proxy_async_global();
+                        }
                         load(sa, &tmA, kb * 64, ti.row0 + arow);
                         if (!B_MN) {
                             const int bbr = args.b_box_rows > 0 ? args.b_box_rows : BN_CTA;
@@ -442,7 +501,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int t = unit; t < total_tiles; t += nunits) {
-                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G);
+                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
                 if (ti.kblocks == 0) continue;
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -470,6 +529,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
+    } else if (DISPATCH && warp >= 2 + Cfg::EPI_WARPS) {
+        // ===================== dispatch (comm warps) =====================
+        const int cw = warp - 2 - Cfg::EPI_WARPS;
+        dispatch_warp<TILE_M>(args, args.K, (int)blockIdx.x * Cfg::COMM_WARPS + cw,
+                              (int)gridDim.x * Cfg::COMM_WARPS, lane);
     } else {
         // ===================== epilogue (warps 2..9) =====================
         const int ew = warp - 2;
@@ -480,7 +544,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = unit; t < total_tiles; t += nunits) {
-            const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G);
+            const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
             const int n0 = ti.n * BN;
             int64_t orow;
             if (K_GROUPED) {

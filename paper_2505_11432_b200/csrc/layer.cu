@@ -10,6 +10,7 @@
 // from the owning rank's input buffer into permuted order; the fc2 epilogue
 // stores each output row into the owning rank's combine staging; device
 // flag barriers (st.release.sys / ld.acquire.sys) separate the phases.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -61,6 +62,8 @@ struct moe_layer {
     uint16_t *x_perm = nullptr, *fc1_out = nullptr, *fc2_in = nullptr, *dy_perm = nullptr,
              *dfc1 = nullptr;
     float *dgate_part = nullptr, *dlogits = nullptr, *rw_part = nullptr;
+    uint32_t* ready = nullptr;     // fused-dispatch arrival counters [Mp / kPad]
+    bool fused_dispatch = true;
     // device pointer tables [n]
     const uint16_t** t_x = nullptr;
     const uint16_t** t_dy = nullptr;
@@ -177,6 +180,17 @@ moe_status build_plans(moe_layer* L) {
     return MOE_OK;
 }
 
+void set_dispatch(moe_layer* L, GemmArgs& a, const uint16_t* const* src, uint16_t* dst) {
+    a.pad_row_tok = L->pad_tok;
+    a.nrows_pad = L->gpad_off + L->el;
+    a.src_bufs = src;
+    a.a_dst = dst;
+    a.ready = L->ready;
+    a.topk = (int)L->k;
+    a.tokens_per_rank = (int)L->Tr;
+    a.err = L->err;
+}
+
 moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
     if (L->n == 1) return MOE_OK;
     if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
@@ -267,6 +281,8 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->dfc1, Mp * 2 * f));
     TRY_ALLOC(dalloc(&L->dgate_part, Mp * (f / 256) * 2));
     TRY_ALLOC(dalloc(&L->dlogits, L->Tr * L->E));
+    TRY_ALLOC(dalloc(&L->ready, Mp / kPad + 1));
+    L->fused_dispatch = getenv("MOE_UNFUSED_DISPATCH") == nullptr;
     TRY_ALLOC(dalloc(&L->rw_part, ((L->Tr + kRwChunk - 1) / kRwChunk) * L->E * h));
     TRY_ALLOC(dalloc(&L->t_x, L->n));
     TRY_ALLOC(dalloc(&L->t_dy, L->n));
@@ -310,7 +326,7 @@ void moe_layer_destroy(moe_layer* L) {
                     L->dropped, L->perm_ws, L->row_map_in, L->out_expert, L->out_src, L->counts,
                     L->expert_off, L->rows, L->gpad_rows, L->gpad_off, L->pad_tok, L->row_dst,
                     L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
-                    L->dgate_part, L->dlogits, L->rw_part, L->t_x, L->t_dy, L->t_stage, L->t_dstage, L->t_ex,
+                    L->dgate_part, L->dlogits, L->rw_part, L->ready, L->t_x, L->t_dy, L->t_stage, L->t_dstage, L->t_ex,
                     L->t_gt, L->t_dgate, L->t_flags, L->err, L->epoch_dev};
     for (void* b : bufs)
         if (b) cudaFree(b);
@@ -395,10 +411,14 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     count_launch();
     // dispatch: AG + local scatter (rows pulled from the owning rank)
     L->mark(PH_DISPATCH, s);
-    dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
-                                                     (int)Tr, (int)h, L->t_x, L->x_perm);
-    count_launch();
-    MOE_CUDA_TRY(cudaGetLastError());
+    if (L->fused_dispatch) {
+        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / kPad + 1) * 4, s));
+    } else {
+        dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
+                                                         (int)Tr, (int)h, L->t_x, L->x_perm);
+        count_launch();
+        MOE_CUDA_TRY(cudaGetLastError());
+    }
     // fc1 + SwiGLU (+ gate before fc2)
     L->mark(PH_FC1, s);
     const bool gate_before = L->cfg.gate_order == MOE_GATE_BEFORE_FC2;
@@ -414,7 +434,10 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         a.out2 = L->fc2_in;
         a.ldo2 = f;
         a.row_gate = gate_before ? L->row_gate : nullptr;
-        MOE_TRY(gemm_launch(L->p_fc1, a, s));
+        set_dispatch(L, a, L->t_x, L->x_perm);
+        GemmPlan p = L->p_fc1;
+        p.dispatch = L->fused_dispatch;
+        MOE_TRY(gemm_launch(p, a, s));
     }
     // fc2 + gather to the source rank's combine staging
     L->mark(PH_FC2, s);
@@ -460,10 +483,14 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     // dgates of dropped (token, slot)s are never written by an expert rank
     MOE_CUDA_TRY(cudaMemsetAsync(L->dgate_sym(), 0, Tr * k * 4, s));
     MOE_TRY(barrier(L, 2, s, 1));
-    // AG(dy) + scatter into permuted order
-    dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
-                                                     (int)Tr, (int)h, L->t_dy, L->dy_perm);
-    count_launch();
+    // AG(dy) + scatter into permuted order (fused into the fc2 dgrad GEMM)
+    if (L->fused_dispatch) {
+        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / kPad + 1) * 4, s));
+    } else {
+        dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
+                                                         (int)Tr, (int)h, L->t_dy, L->dy_perm);
+        count_launch();
+    }
     // fc2 dgrad fused with SwiGLU/gate backward and remat of fc2_in
     L->mark(PH_FC2_DGRAD, s);
     {
@@ -481,7 +508,10 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.ld_aux = 2 * f;
         a.row_gate = L->row_gate;
         a.row_part = L->dgate_part;
-        MOE_TRY(gemm_launch(L->p_fc2_dgrad, a, s));
+        set_dispatch(L, a, L->t_dy, L->dy_perm);
+        GemmPlan p = L->p_fc2_dgrad;
+        p.dispatch = L->fused_dispatch;
+        MOE_TRY(gemm_launch(p, a, s));
     }
     // fc1 dgrad + gather of dx rows to the owning rank (GEMM + RS)
     L->mark(PH_FC1_DGRAD, s);
