@@ -10,7 +10,7 @@ HDR := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/moe_b20
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 LIB := $(PKG)/libmoe_b200.so
 
-all: $(LIB) oracle
+all: $(LIB) compat oracle
 
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build
@@ -22,7 +22,25 @@ $(LIB): $(OBJ)
 oracle:
 	$(MAKE) -C oracle all
 
+# Drop-in C++ adapter with the reference's routing.hpp signatures (built
+# against the reference's own header when the tree is present; the .so and
+# the reference-test binary travel prebuilt).
+REF ?= /root/reference/proj
+JSON_INC ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
+COMPAT := $(PKG)/libmoeplan_compat.so
+compat: $(LIB)
+	@if [ -d "$(REF)/core/include" ]; then \
+	  g++ -std=c++20 -O2 -fPIC -shared -Ioracle/shim -I$(JSON_INC) -I$(REF)/core/include \
+	    -I/usr/local/cuda/include -o $(COMPAT) $(PKG)/compat/moeplan_compat.cpp \
+	    -L$(PKG) -lmoe_b200 -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN' && \
+	  mkdir -p oracle/_ref && \
+	  g++ -std=c++20 -O2 -Itests/doctest_shim -Ioracle/shim -I$(JSON_INC) -I$(REF)/core/include \
+	    -I$(REF)/tests -o oracle/_ref/ref_test_routing_on_gpu $(REF)/tests/test_routing.cpp \
+	    -L$(PKG) -lmoeplan_compat -lmoe_b200 -L/usr/local/cuda/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' && echo "built compat adapter + reference test binary"; \
+	else echo "reference headers absent: using prebuilt $(COMPAT)"; fi
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all oracle clean
+.PHONY: all oracle compat clean

@@ -248,6 +248,30 @@ def run_ours(args, cfg):
     ms = float(t.item())
     value = n * Tr / (ms / 1000.0)
 
+    # ---- exposed communication: T_layer - T_compute_only (schedule.cpp:149-152) ----
+    exposed = None
+    if world > 1:
+        L.set_compute_only(True)
+        for _ in range(2):
+            step()
+        sync_all()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(args.steps):
+            step()
+        c1.record(stream)
+        sync_all()
+        tc = torch.tensor([c0.elapsed_time(c1) / args.steps], device="cuda")
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        L.set_compute_only(False)
+        for _ in range(2):
+            step()
+        sync_all()
+        comp_ms = float(tc.item())
+        exposed = {"t_layer_ms": ms, "t_compute_only_ms": comp_ms,
+                   "exposed_ms": ms - comp_ms, "exposed_pct": 100.0 * (ms - comp_ms) / ms,
+                   "definition": "T_layer - T_compute_only (same kernels, peer buffers replaced by local ones, no barriers), max over ranks"}
+
     # ---- per-phase device times (one instrumented step, same stream) ----
     L.enable_timing(True)
     phases = {}
@@ -343,6 +367,7 @@ def run_ours(args, cfg):
                          "step_frac": total_flops / (ms / 1000.0) / 1e12 / peaks["bf16_sus"]},
             "phases_ms": {kk: round(v, 4) for kk, v in phases.items()},
             "routing_rank0": routing_info,
+            "exposed_comm": exposed,
             "clocks": clk,
             "gpu_launches": int(launches),
             "gpu_launches_per_step": int(per_step_launches),

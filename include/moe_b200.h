@@ -223,6 +223,13 @@ moe_status moe_layer_enable_timing(moe_layer* L, int enable);
 moe_status moe_layer_phase_times(moe_layer* L, float* h_ms, int max_phases, int* n_phases,
                                  const char** names);
 
+/* Measurement mode for exposed communication (reference definition
+ * exposed = makespan - busy_compute, schedule.cpp:149-152): compute_only = 1
+ * runs the identical kernel sequence with every peer buffer replaced by
+ * this rank's own (no NVLink traffic, no cross-GPU barriers). Results are
+ * not meaningful in that mode; 0 restores normal operation. */
+moe_status moe_layer_set_comm_mode(moe_layer* L, int compute_only);
+
 /* Non-zero if a cross-GPU flag wait of this layer timed out (synchronous). */
 int moe_layer_error_flag(moe_layer* L);
 

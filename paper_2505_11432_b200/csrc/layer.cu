@@ -73,6 +73,18 @@ struct moe_layer {
     float** t_gt = nullptr;
     float** t_dgate = nullptr;
     uint32_t** t_flags = nullptr;
+    // compute-only emulation: every table entry points at this rank's arena
+    const uint16_t** l_x = nullptr;
+    const uint16_t** l_dy = nullptr;
+    void** l_stage = nullptr;
+    void** l_dstage = nullptr;
+    float** l_dgate = nullptr;
+    bool comm_local = false;
+    const uint16_t* const* tx() const { return comm_local ? l_x : t_x; }
+    const uint16_t* const* tdy() const { return comm_local ? l_dy : t_dy; }
+    void* const* tstage() const { return comm_local ? l_stage : t_stage; }
+    void* const* tdstage() const { return comm_local ? l_dstage : t_dstage; }
+    float* const* tdgate() const { return comm_local ? l_dgate : t_dgate; }
     int* err = nullptr;
     uint32_t* epoch_dev = nullptr;
     bool router_attr = false;
@@ -135,6 +147,18 @@ moe_status fill_tables(moe_layer* L) {
     MOE_CUDA_TRY(cudaMemcpy(L->t_gt, tg.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
     MOE_CUDA_TRY(cudaMemcpy(L->t_dgate, tdg.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
     MOE_CUDA_TRY(cudaMemcpy(L->t_flags, tf.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    for (int p = 0; p < n; ++p) {
+        tx[p] = tx[L->rank];
+        tdy[p] = tdy[L->rank];
+        ts[p] = ts[L->rank];
+        tds[p] = tds[L->rank];
+        tdg[p] = tdg[L->rank];
+    }
+    MOE_CUDA_TRY(cudaMemcpy(L->l_x, tx.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->l_dy, tdy.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->l_stage, ts.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->l_dstage, tds.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->l_dgate, tdg.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
     return MOE_OK;
 }
 
@@ -192,7 +216,7 @@ void set_dispatch(moe_layer* L, GemmArgs& a, const uint16_t* const* src, uint16_
 }
 
 moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
-    if (L->n == 1) return MOE_OK;
+    if (L->n == 1 || L->comm_local) return MOE_OK;
     if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
     flag_barrier_kernel<<<1, 64, 0, s>>>(L->t_flags, slot, (int)L->n, (int)L->rank, L->epoch_dev,
                                         bump, 20ull * 1000 * 1000 * 1000, L->err);
@@ -292,6 +316,11 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->t_gt, L->n));
     TRY_ALLOC(dalloc(&L->t_dgate, L->n));
     TRY_ALLOC(dalloc(&L->t_flags, L->n));
+    TRY_ALLOC(dalloc(&L->l_x, L->n));
+    TRY_ALLOC(dalloc(&L->l_dy, L->n));
+    TRY_ALLOC(dalloc(&L->l_stage, L->n));
+    TRY_ALLOC(dalloc(&L->l_dstage, L->n));
+    TRY_ALLOC(dalloc(&L->l_dgate, L->n));
     TRY_ALLOC(dalloc(&L->err, 1));
     cudaMemset(L->err, 0, sizeof(int));
     TRY_ALLOC(dalloc(&L->epoch_dev, 1));
@@ -327,7 +356,7 @@ void moe_layer_destroy(moe_layer* L) {
                     L->expert_off, L->rows, L->gpad_rows, L->gpad_off, L->pad_tok, L->row_dst,
                     L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
                     L->dgate_part, L->dlogits, L->rw_part, L->ready, L->t_x, L->t_dy, L->t_stage, L->t_dstage, L->t_ex,
-                    L->t_gt, L->t_dgate, L->t_flags, L->err, L->epoch_dev};
+                    L->t_gt, L->t_dgate, L->t_flags, L->l_x, L->l_dy, L->l_stage, L->l_dstage, L->l_dgate, L->err, L->epoch_dev};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
@@ -392,7 +421,8 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     }
     // routing metadata all-gather over NVLink
     publish_meta_kernel<<<std::min<int64_t>((Tr * k + 255) / 256, 64), 256, 0, s>>>(
-        L->ex_loc, L->gt_loc, (int)(Tr * k), (int)(L->rank * Tr * k), L->t_ex, L->t_gt, (int)L->n);
+        L->ex_loc, L->gt_loc, (int)(Tr * k), (int)(L->rank * Tr * k), L->t_ex + (L->comm_local ? L->rank : 0),
+        L->t_gt + (L->comm_local ? L->rank : 0), L->comm_local ? 1 : (int)L->n);
     count_launch();
     MOE_TRY(barrier(L, 0, s, 1));
     L->mark(PH_PERMUTE, s);
@@ -415,7 +445,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / kPad + 1) * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
-                                                         (int)Tr, (int)h, L->t_x, L->x_perm);
+                                                         (int)Tr, (int)h, L->tx(), L->x_perm);
         count_launch();
         MOE_CUDA_TRY(cudaGetLastError());
     }
@@ -434,7 +464,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         a.out2 = L->fc2_in;
         a.ldo2 = f;
         a.row_gate = gate_before ? L->row_gate : nullptr;
-        set_dispatch(L, a, L->t_x, L->x_perm);
+        set_dispatch(L, a, L->tx(), L->x_perm);
         GemmPlan p = L->p_fc1;
         p.dispatch = L->fused_dispatch;
         MOE_TRY(gemm_launch(p, a, s));
@@ -450,7 +480,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         a.b_group_stride = (int)h;
         a.ldo = h;
         a.row_dst = L->row_dst;
-        a.rank_base = L->t_stage;
+        a.rank_base = L->tstage();
         a.row_gate = L->row_gate;
         a.gate_rows = gate_before ? 0 : 1;
         MOE_TRY(gemm_launch(L->p_fc2, a, s));
@@ -488,7 +518,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / kPad + 1) * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
-                                                         (int)Tr, (int)h, L->t_dy, L->dy_perm);
+                                                         (int)Tr, (int)h, L->tdy(), L->dy_perm);
         count_launch();
     }
     // fc2 dgrad fused with SwiGLU/gate backward and remat of fc2_in
@@ -508,7 +538,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.ld_aux = 2 * f;
         a.row_gate = L->row_gate;
         a.row_part = L->dgate_part;
-        set_dispatch(L, a, L->t_dy, L->dy_perm);
+        set_dispatch(L, a, L->tdy(), L->dy_perm);
         GemmPlan p = L->p_fc2_dgrad;
         p.dispatch = L->fused_dispatch;
         MOE_TRY(gemm_launch(p, a, s));
@@ -524,12 +554,12 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.b_group_stride = (int)(2 * f);
         a.ldo = h;
         a.row_dst = L->row_dst;
-        a.rank_base = L->t_dstage;
+        a.rank_base = L->tdstage();
         MOE_TRY(gemm_launch(L->p_fc1_dgrad, a, s));
     }
     L->mark(PH_DGATE, s);
     dgate_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgate_part, (int)(f / 256) * 2, L->row_dst,
-                                                L->gpad_off + el, L->t_dgate);
+                                                L->gpad_off + el, L->tdgate());
     count_launch();
     MOE_TRY(barrier(L, 3, s, 0));
     L->mark(PH_COMBINE_DX, s);
@@ -660,6 +690,12 @@ moe_status moe_layer_ipc_import(moe_layer* L, const void* h_blobs) {
     }
     MOE_TRY(fill_tables(L));
     L->ipc_ready = true;
+    return MOE_OK;
+}
+
+moe_status moe_layer_set_comm_mode(moe_layer* L, int compute_only) {
+    MOE_CHECK_ARG(L, "null argument");
+    L->comm_local = compute_only != 0;
     return MOE_OK;
 }
 

@@ -151,6 +151,10 @@ class MoELayer:
         check(lib().moe_layer_phase_times(self._h, ms, 32, C.byref(cnt), names))
         return {names[i].decode(): ms[i] for i in range(cnt.value)}
 
+    def set_compute_only(self, on: bool):
+        """Exposed-comm measurement mode (see moe_layer_set_comm_mode)."""
+        check(lib().moe_layer_set_comm_mode(self._h, int(bool(on))))
+
     def error_flag(self) -> int:
         return int(lib().moe_layer_error_flag(self._h))
 

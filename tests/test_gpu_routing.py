@@ -125,3 +125,18 @@ def test_router_topk_vs_oracle():
     clear = (s[:, k - 1] - s[:, k]) > 1e-3
     assert (ex.cpu().numpy()[clear] == oex[clear]).all()
     np.testing.assert_allclose(g.cpu().numpy()[clear], og[clear], rtol=1e-4, atol=1e-5)
+
+
+def test_reference_test_routing_against_gpu_adapter():
+    """The reference's own tests/test_routing.cpp, compiled unmodified against
+    the drop-in adapter (libmoeplan_compat.so -> sm_100a kernels)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "ref_test_routing_on_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("reference test binary not built (needs /root/reference at build time)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(p.stdout[-2000:])
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+    assert "0 failed" in p.stdout
