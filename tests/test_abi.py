@@ -33,7 +33,7 @@ def test_compat_adapter_exports():
         pytest.skip("compat adapter not built")
     out = os.popen(f"nm -DC {path}").read()
     for sym in ("moeplan::routing::build_scatter_map", "moeplan::routing::sort_tokens_for_tiles",
-                "moeplan::routing::balance_metrics", "moeplan::numerics::quantize"):
+                "moeplan::routing::balance_metrics", "moeplan::routing::simulate_routing"):
         assert sym in out, sym
 
 
