@@ -5,6 +5,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -231,6 +232,20 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 __device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
     __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&v);
     return __bfloat1622float2(b);
+}
+
+// E4M3 pack/unpack (RNE, saturating to +-448; the FP8 communication format,
+// PAPER.md:359-360). lo goes to the low byte.
+__device__ __forceinline__ uint16_t f32x2_to_e4m3x2(float lo, float hi) {
+    uint16_t r;
+    asm("{cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;}" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ float2 e4m3x2_to_f32x2(uint16_t v) {
+    uint32_t h2;
+    asm("{cvt.rn.f16x2.e4m3x2 %0, %1;}" : "=r"(h2) : "h"(v));
+    __half2 hh = *reinterpret_cast<__half2*>(&h2);
+    return __half22float2(hh);
 }
 
 // --- system-scope flags for cross-GPU signalling ----------------------------

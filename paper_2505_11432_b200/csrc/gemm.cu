@@ -62,6 +62,8 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s) {
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_SCATTER)      // fc2 + gather
     MOE_GEMM_CASE(256, 2, false, true, false, EPI_SWIGLU_BWD)    // fc2 dgrad
     MOE_GEMM_CASE(256, 2, false, true, false, EPI_SCATTER)       // fc1 dgrad
+    MOE_GEMM_CASE(256, 2, false, false, false, EPI_SCATTER_FP8)  // fc2 + FP8 combine payload
+    MOE_GEMM_CASE(256, 2, false, true, false, EPI_SCATTER_FP8)   // fc1 dgrad + FP8 payload
     MOE_GEMM_CASE(256, 2, true, true, true, EPI_STORE_BF16)      // wgrads
     MOE_GEMM_CASE(256, 2, true, true, true, EPI_STORE_F32)
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_STORE_BF16)   // generic

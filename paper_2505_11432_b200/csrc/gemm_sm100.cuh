@@ -36,6 +36,7 @@ enum EpiKind : int {
     EPI_SWIGLU = 2,       // fc1: store fc1_out (bf16) and fc2_in = a*silu(b)*gate
     EPI_SCATTER = 3,      // fc2 / fc1-dgrad: rows -> (rank, slot row) staging
     EPI_SWIGLU_BWD = 4,   // fc2-dgrad: SwiGLU+gate backward, remat fc2_in, dgate partials
+    EPI_SCATTER_FP8 = 5,  // EPI_SCATTER with grouped-128 E4M3 payload + fp32 scales (FP8 comm)
 };
 
 struct GemmArgs {
@@ -67,6 +68,12 @@ struct GemmArgs {
     uint32_t* ready;                    // [padded rows / TILE_M] rows landed per tile block
     int topk, tokens_per_rank;
     int* err;                           // set to 2 on a dispatch wait timeout
+    // FP8 communication
+    const uint8_t* const* src_bufs8;    // per source rank: E4M3 token rows [T_r, K]
+    const float* const* src_scales;     // per source rank: scales [T_r, K / src_scale_group]
+    int src_scale_group;                // K (per-token) or 128 (grouped)
+    const float* row_scale;             // optional extra per-permuted-row factor (gate)
+    void* const* rank_scale_base;       // SCATTER_FP8: per destination rank scale base
 };
 
 template <int BN, int CG>
@@ -229,6 +236,45 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                 }
             }
         }
+    } else if constexpr (EPI == EPI_SCATTER_FP8) {
+        // one warp-half = one 128-column group: absmax pass over TMEM, then
+        // quantise pass; codes + one fp32 scale per (row, group) go to the
+        // owning rank's staging (grouped-128 E4M3, numerics.cpp:88-160)
+        static_assert(HALF == 128, "FP8 scatter needs 128-column groups");
+        const int dst = args.row_dst[orow];
+        float amax = 0.0f;
+#pragma unroll 1
+        for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tbase + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(__uint_as_float(r[i])));
+        }
+        const float scale = amax > 0.0f ? amax / 448.0f : 1.0f;
+        const float inv = 1.0f / scale;
+        uint8_t* codes = nullptr;
+        if (dst >= 0) {
+            const int64_t drow = dst & ((1 << 27) - 1);
+            codes = reinterpret_cast<uint8_t*>(args.rank_base[dst >> 27]) + drow * args.ldo + n0;
+            reinterpret_cast<float*>(args.rank_scale_base[dst >> 27])[drow * (args.ldo / 128) + (n0 + c_lo) / 128] = scale;
+        }
+#pragma unroll 1
+        for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tbase + c0, r);
+            tmem_ld_wait();
+            if (dst < 0) continue;
+            uint32_t pk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint16_t lo = f32x2_to_e4m3x2(__uint_as_float(r[4 * q]) * inv, __uint_as_float(r[4 * q + 1]) * inv);
+                const uint16_t hi = f32x2_to_e4m3x2(__uint_as_float(r[4 * q + 2]) * inv, __uint_as_float(r[4 * q + 3]) * inv);
+                pk[q] = (uint32_t)lo | ((uint32_t)hi << 16);
+            }
+            *reinterpret_cast<uint4*>(codes + c0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(codes + c0 + 16) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
     } else if constexpr (EPI == EPI_SWIGLU) {
         // accumulator cols [0,BN/2) = a block, [BN/2,BN) = b block (W1 rows
         // interleaved per BN/2 block at weight-pack time); this warp takes
@@ -341,12 +387,45 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid,
         uint4* d = reinterpret_cast<uint4*>(a.a_dst + (int64_t)pp * K);
         if (i < 0) {
             for (int v = lane; v < nvec; v += 32) d[v] = make_uint4(0, 0, 0, 0);
+        } else if (a.src_bufs8) {
+            // FP8 pull: 16 E4M3 codes per lane-step -> dequantise -> 2 x 16 B bf16
+            const int t = i / a.topk;
+            const int src = t / a.tokens_per_rank;
+            const int tl = t - src * a.tokens_per_rank;
+            const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs8[src] + (int64_t)tl * K);
+            const float* sc = a.src_scales[src] + (int64_t)tl * (K / a.src_scale_group);
+            const float rs = a.row_scale ? a.row_scale[pp] : 1.0f;
+            for (int v = lane; v < K / 16; v += 32) {
+                const uint4 c = sp[v];
+                const float f = sc[(v * 16) / a.src_scale_group] * rs;
+                const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+                uint32_t o[8];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 lo = e4m3x2_to_f32x2((uint16_t)(w[q] & 0xffff));
+                    const float2 hi = e4m3x2_to_f32x2((uint16_t)(w[q] >> 16));
+                    o[2 * q] = pack_bf16x2(lo.x * f, lo.y * f);
+                    o[2 * q + 1] = pack_bf16x2(hi.x * f, hi.y * f);
+                }
+                d[2 * v] = make_uint4(o[0], o[1], o[2], o[3]);
+                d[2 * v + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+            }
         } else {
             const int t = i / a.topk;
             const int src = t / a.tokens_per_rank;
             const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs[src] +
                                                              (int64_t)(t - src * a.tokens_per_rank) * K);
             int v = lane;
+            if (a.row_scale) {
+                const float rs = a.row_scale[pp];
+                for (; v < nvec; v += 32) {
+                    const uint4 c = sp[v];
+                    const float2 p0 = unpack_bf16x2(c.x), p1 = unpack_bf16x2(c.y),
+                                 p2 = unpack_bf16x2(c.z), p3 = unpack_bf16x2(c.w);
+                    d[v] = make_uint4(pack_bf16x2(p0.x * rs, p0.y * rs), pack_bf16x2(p1.x * rs, p1.y * rs),
+                                      pack_bf16x2(p2.x * rs, p2.y * rs), pack_bf16x2(p3.x * rs, p3.y * rs));
+                }
+            }
             for (; v + 224 < nvec; v += 256) {
                 uint4 r[8];
 #pragma unroll

@@ -7,9 +7,13 @@
 // Multi-GPU (ep_size = n > 1): one process per GPU. Every rank owns one
 // symmetric arena (identical offsets on every rank) exported with CUDA IPC;
 // peers' arenas are mapped over NVLink. Dispatch pulls token rows straight
-// from the owning rank's input buffer into permuted order; the fc2 epilogue
-// stores each output row into the owning rank's combine staging; device
-// flag barriers (st.release.sys / ld.acquire.sys) separate the phases.
+// from the owning rank's input buffer into permuted order inside the fc1 /
+// fc2-dgrad GEMM (fused AG + scatter); the fc2 / fc1-dgrad epilogues store
+// each output row into the owning rank's combine staging (fused gather +
+// RS); device flag barriers (st.release.sys / ld.acquire.sys) separate the
+// phases. FP8 communication sends E4M3 codes + fp32
+// scales on all four exchanges: per-token for the forward dispatch,
+// grouped-128 for the combine payloads and the backward dispatch.
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -25,6 +29,12 @@ namespace {
 size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
 constexpr int kCG = 2;          // CTA-pair GEMMs
 constexpr int kPad = 128 * kCG;  // expert row segments padded to the tile height
+
+// fields of the symmetric arena (same offsets on every rank)
+enum Field {
+    F_X, F_DY, F_STAGE, F_DSTAGE, F_EX, F_GT, F_DGATE, F_FLAGS,
+    F_X8, F_XSC, F_DY8, F_DYSC, F_STAGE8, F_SSC, F_DSTAGE8, F_DSSC, F_COUNT
+};
 }  // namespace
 
 enum Phase {
@@ -42,12 +52,17 @@ struct moe_layer {
     moe_layer_config cfg{};
     int64_t Tr = 0, T = 0, h = 0, f = 0, E = 0, k = 0, n = 1, rank = 0, el = 0, first = 0, Mp = 0;
     int dev = 0;
+    bool fp8 = false, gate_after = false;
     // symmetric arena (IPC-exported)
     uint8_t* arena = nullptr;
     size_t arena_bytes = 0;
-    size_t off_x = 0, off_dy = 0, off_stage = 0, off_dstage = 0, off_ex = 0, off_gt = 0,
-           off_dgate = 0, off_flags = 0;
+    size_t off[moe::F_COUNT] = {};
     std::vector<uint8_t*> peer_arena;  // [n], self included
+    // per-field pointer tables [F_COUNT][n]: remote (peers' arenas) and
+    // local (every entry = this rank: compute-only measurement mode)
+    void** tab_remote = nullptr;
+    void** tab_local = nullptr;
+    bool comm_local = false;
     // local buffers
     uint16_t *w1p = nullptr, *w2 = nullptr, *wr = nullptr;
     int32_t* ex_loc = nullptr;
@@ -62,47 +77,26 @@ struct moe_layer {
     uint16_t *x_perm = nullptr, *fc1_out = nullptr, *fc2_in = nullptr, *dy_perm = nullptr,
              *dfc1 = nullptr;
     float *dgate_part = nullptr, *dlogits = nullptr, *rw_part = nullptr;
-    uint32_t* ready = nullptr;     // fused-dispatch arrival counters [Mp / kPad]
+    uint32_t* ready = nullptr;  // fused-dispatch arrival counters [Mp / kPad]
     bool fused_dispatch = true;
-    // device pointer tables [n]
-    const uint16_t** t_x = nullptr;
-    const uint16_t** t_dy = nullptr;
-    void** t_stage = nullptr;
-    void** t_dstage = nullptr;
-    int32_t** t_ex = nullptr;
-    float** t_gt = nullptr;
-    float** t_dgate = nullptr;
-    uint32_t** t_flags = nullptr;
-    // compute-only emulation: every table entry points at this rank's arena
-    const uint16_t** l_x = nullptr;
-    const uint16_t** l_dy = nullptr;
-    void** l_stage = nullptr;
-    void** l_dstage = nullptr;
-    float** l_dgate = nullptr;
-    bool comm_local = false;
-    const uint16_t* const* tx() const { return comm_local ? l_x : t_x; }
-    const uint16_t* const* tdy() const { return comm_local ? l_dy : t_dy; }
-    void* const* tstage() const { return comm_local ? l_stage : t_stage; }
-    void* const* tdstage() const { return comm_local ? l_dstage : t_dstage; }
-    float* const* tdgate() const { return comm_local ? l_dgate : t_dgate; }
     int* err = nullptr;
     uint32_t* epoch_dev = nullptr;
     bool router_attr = false;
     bool weights_set = false, routing_set = false, fwd_done = false, ipc_ready = false;
-    // GEMM plans (tensor maps fixed at create / set_weights)
+    // GEMM plans (tensor maps fixed at create)
     moe::GemmPlan p_fc1, p_fc2, p_fc2_dgrad, p_fc2_wgrad, p_fc1_dgrad, p_fc1_wgrad;
     // timing
     bool timing = false;
     cudaEvent_t ev[moe::PH_COUNT] = {};
     bool ev_used[moe::PH_COUNT] = {};
 
-    uint16_t* x_sym() { return reinterpret_cast<uint16_t*>(arena + off_x); }
-    uint16_t* dy_sym() { return reinterpret_cast<uint16_t*>(arena + off_dy); }
-    uint16_t* stage_sym() { return reinterpret_cast<uint16_t*>(arena + off_stage); }
-    uint16_t* dstage_sym() { return reinterpret_cast<uint16_t*>(arena + off_dstage); }
-    int32_t* ex_all() { return reinterpret_cast<int32_t*>(arena + off_ex); }
-    float* gt_all() { return reinterpret_cast<float*>(arena + off_gt); }
-    float* dgate_sym() { return reinterpret_cast<float*>(arena + off_dgate); }
+    template <class T>
+    T* mine(int field) { return reinterpret_cast<T*>(arena + off[field]); }
+    // device array of n per-rank pointers for `field`
+    template <class T>
+    T* const* tab(int field) const {
+        return reinterpret_cast<T* const*>((comm_local ? tab_local : tab_remote) + field * n);
+    }
     void mark(int ph, cudaStream_t s) {
         if (timing) {
             cudaEventRecord(ev[ph], s);
@@ -123,42 +117,14 @@ moe_status dalloc(T** p, size_t count) {
 
 moe_status fill_tables(moe_layer* L) {
     const int n = (int)L->n;
-    std::vector<const uint16_t*> tx(n), tdy(n);
-    std::vector<void*> ts(n), tds(n);
-    std::vector<int32_t*> te(n);
-    std::vector<float*> tg(n), tdg(n);
-    std::vector<uint32_t*> tf(n);
-    for (int p = 0; p < n; ++p) {
-        uint8_t* a = L->peer_arena[p];
-        tx[p] = reinterpret_cast<const uint16_t*>(a + L->off_x);
-        tdy[p] = reinterpret_cast<const uint16_t*>(a + L->off_dy);
-        ts[p] = a + L->off_stage;
-        tds[p] = a + L->off_dstage;
-        te[p] = reinterpret_cast<int32_t*>(a + L->off_ex);
-        tg[p] = reinterpret_cast<float*>(a + L->off_gt);
-        tdg[p] = reinterpret_cast<float*>(a + L->off_dgate);
-        tf[p] = reinterpret_cast<uint32_t*>(a + L->off_flags);
-    }
-    MOE_CUDA_TRY(cudaMemcpy(L->t_x, tx.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->t_dy, tdy.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->t_stage, ts.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->t_dstage, tds.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->t_ex, te.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->t_gt, tg.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->t_dgate, tdg.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->t_flags, tf.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    for (int p = 0; p < n; ++p) {
-        tx[p] = tx[L->rank];
-        tdy[p] = tdy[L->rank];
-        ts[p] = ts[L->rank];
-        tds[p] = tds[L->rank];
-        tdg[p] = tdg[L->rank];
-    }
-    MOE_CUDA_TRY(cudaMemcpy(L->l_x, tx.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->l_dy, tdy.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->l_stage, ts.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->l_dstage, tds.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
-    MOE_CUDA_TRY(cudaMemcpy(L->l_dgate, tdg.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    std::vector<void*> remote(F_COUNT * n), local(F_COUNT * n);
+    for (int fld = 0; fld < F_COUNT; ++fld)
+        for (int p = 0; p < n; ++p) {
+            remote[fld * n + p] = L->peer_arena[p] + L->off[fld];
+            local[fld * n + p] = L->arena + L->off[fld];
+        }
+    MOE_CUDA_TRY(cudaMemcpy(L->tab_remote, remote.data(), sizeof(void*) * remote.size(), cudaMemcpyHostToDevice));
+    MOE_CUDA_TRY(cudaMemcpy(L->tab_local, local.data(), sizeof(void*) * local.size(), cudaMemcpyHostToDevice));
     return MOE_OK;
 }
 
@@ -171,7 +137,7 @@ moe_status build_plans(moe_layer* L) {
     MOE_TRY(tmap_kmajor(&L->p_fc1.tb, L->w1p, el * 2 * f, h, 256 / kCG));
     // forward fc2: A = fc2_in [Mp, f], B = w2 [el*h, f] (K-major)
     L->p_fc2 = GemmPlan{};
-    L->p_fc2.epi = EPI_SCATTER;
+    L->p_fc2.epi = L->fp8 ? EPI_SCATTER_FP8 : EPI_SCATTER;
     MOE_TRY(tmap_kmajor(&L->p_fc2.ta, L->fc2_in, Mp, f, 128));
     MOE_TRY(tmap_kmajor(&L->p_fc2.tb, L->w2, el * h, f, 256 / kCG));
     // fc2 dgrad: A = dy_perm [Mp, h], B(n=f, k=h) = w2[e][k][n] (MN-major)
@@ -188,7 +154,7 @@ moe_status build_plans(moe_layer* L) {
     MOE_TRY(tmap_mnmajor(&L->p_fc2_wgrad.tb, L->fc2_in, Mp, f));
     // fc1 dgrad: A = dfc1 [Mp, 2f], B(n=h, k=j) = w1p[e][j][n] (MN-major)
     L->p_fc1_dgrad = GemmPlan{};
-    L->p_fc1_dgrad.epi = EPI_SCATTER;
+    L->p_fc1_dgrad.epi = L->fp8 ? EPI_SCATTER_FP8 : EPI_SCATTER;
     L->p_fc1_dgrad.b_mn = true;
     MOE_TRY(tmap_kmajor(&L->p_fc1_dgrad.ta, L->dfc1, Mp, 2 * f, 128));
     MOE_TRY(tmap_mnmajor(&L->p_fc1_dgrad.tb, L->w1p, el * 2 * f, h));
@@ -204,22 +170,51 @@ moe_status build_plans(moe_layer* L) {
     return MOE_OK;
 }
 
-void set_dispatch(moe_layer* L, GemmArgs& a, const uint16_t* const* src, uint16_t* dst) {
+// Fused dispatch (AG + local scatter) of one of the two pulled operands.
+void set_dispatch(moe_layer* L, GemmArgs& a, bool backward, uint16_t* dst) {
     a.pad_row_tok = L->pad_tok;
     a.nrows_pad = L->gpad_off + L->el;
-    a.src_bufs = src;
     a.a_dst = dst;
     a.ready = L->ready;
     a.topk = (int)L->k;
     a.tokens_per_rank = (int)L->Tr;
     a.err = L->err;
+    if (!backward) {
+        a.src_bufs = L->tab<const uint16_t>(F_X);
+        if (L->fp8) {
+            a.src_bufs8 = L->tab<const uint8_t>(F_X8);
+            a.src_scales = L->tab<const float>(F_XSC);
+            a.src_scale_group = (int)L->h;  // per-token
+        }
+    } else {
+        a.src_bufs = L->tab<const uint16_t>(F_DY);
+        if (L->fp8) {
+            a.src_bufs8 = L->tab<const uint8_t>(F_DY8);
+            a.src_scales = L->tab<const float>(F_DYSC);
+            a.src_scale_group = 128;        // grouped-128 in backward
+        }
+        // gate after fc2: d fc2_out = gate * dy
+        if (L->gate_after) a.row_scale = L->row_gate;
+    }
 }
 
 moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
     if (L->n == 1 || L->comm_local) return MOE_OK;
     if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
-    flag_barrier_kernel<<<1, 64, 0, s>>>(L->t_flags, slot, (int)L->n, (int)L->rank, L->epoch_dev,
-                                        bump, 20ull * 1000 * 1000 * 1000, L->err);
+    flag_barrier_kernel<<<1, 64, 0, s>>>(L->tab<uint32_t>(F_FLAGS), slot, (int)L->n, (int)L->rank,
+                                        L->epoch_dev, bump, 20ull * 1000 * 1000 * 1000, L->err);
+    count_launch();
+    MOE_CUDA_TRY(cudaGetLastError());
+    return MOE_OK;
+}
+
+moe_status quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, bool per_token,
+                         uint8_t* codes, float* scales, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>((rows + 7) / 8, kNumSMs * 8);
+    if (per_token)
+        quantize_fast_kernel<0><<<grid, 256, 0, s>>>(x, (int)rows, (int)cols, codes, scales);
+    else
+        quantize_fast_kernel<128><<<grid, 256, 0, s>>>(x, (int)rows, (int)cols, codes, scales);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;
@@ -242,9 +237,14 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
                   "num_experts must be divisible by ep_size (<= 32)");
     MOE_CHECK_ARG(c.rank >= 0 && c.rank < c.ep_size, "rank out of range");
     MOE_CHECK_ARG(c.num_experts / c.ep_size <= 256, "at most 256 local experts");
-    MOE_CHECK_ARG(c.comm_format == MOE_COMM_BF16, "FP8 communication is not enabled in this build of the layer");
+    MOE_CHECK_ARG(c.comm_format == MOE_COMM_BF16 || c.comm_format == MOE_COMM_FP8,
+                  "comm_format must be bf16 or fp8");
+    MOE_CHECK_ARG(c.gate_order == MOE_GATE_BEFORE_FC2 || c.gate_order == MOE_GATE_AFTER_FC2,
+                  "gate_order must be before_fc2_in or after_fc2_out");
     auto* L = new moe_layer();
     L->cfg = c;
+    L->fp8 = c.comm_format == MOE_COMM_FP8;
+    L->gate_after = c.gate_order == MOE_GATE_AFTER_FC2;
     L->Tr = c.tokens_per_rank;
     L->n = c.ep_size;
     L->rank = c.rank;
@@ -260,36 +260,49 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     cudaGetDevice(&L->dev);
 
     // ---- symmetric arena ----
-    size_t off = 0;
-    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
-    L->off_x = take(L->Tr * L->h * 2);
-    L->off_dy = take(L->Tr * L->h * 2);
-    L->off_stage = take(L->Tr * L->k * L->h * 2);
-    L->off_dstage = take(L->Tr * L->k * L->h * 2);
-    L->off_ex = take(L->T * L->k * 4);
-    L->off_gt = take(L->T * L->k * 4);
-    L->off_dgate = take(L->Tr * L->k * 4);
-    L->off_flags = take(16 * 64 * 4);
-    L->arena_bytes = off;
+    const int64_t Tr = L->Tr, h = L->h, k = L->k;
+    size_t sizes[F_COUNT] = {};
+    sizes[F_X] = Tr * h * 2;
+    sizes[F_DY] = Tr * h * 2;
+    sizes[F_STAGE] = Tr * k * h * 2;
+    sizes[F_DSTAGE] = Tr * k * h * 2;
+    sizes[F_EX] = L->T * k * 4;
+    sizes[F_GT] = L->T * k * 4;
+    sizes[F_DGATE] = Tr * k * 4;
+    sizes[F_FLAGS] = 16 * 64 * 4;
+    sizes[F_X8] = L->fp8 ? Tr * h : 0;
+    sizes[F_XSC] = L->fp8 ? Tr * 4 : 0;
+    sizes[F_DY8] = L->fp8 ? Tr * h : 0;
+    sizes[F_DYSC] = L->fp8 ? Tr * (h / 128) * 4 : 0;
+    sizes[F_STAGE8] = L->fp8 ? Tr * k * h : 0;
+    sizes[F_SSC] = L->fp8 ? Tr * k * (h / 128) * 4 : 0;
+    sizes[F_DSTAGE8] = L->fp8 ? Tr * k * h : 0;
+    sizes[F_DSSC] = L->fp8 ? Tr * k * (h / 128) * 4 : 0;
+    size_t total = 0;
+    for (int fld = 0; fld < F_COUNT; ++fld) {
+        L->off[fld] = total;
+        total = align_up(total + sizes[fld]);
+    }
+    L->arena_bytes = total;
     moe_status st = MOE_OK;
 #define TRY_ALLOC(expr) do { st = (expr); if (st != MOE_OK) { moe_layer_destroy(L); return st; } } while (0)
     TRY_ALLOC(dalloc(&L->arena, L->arena_bytes));
     cudaMemset(L->arena, 0, L->arena_bytes);
     L->peer_arena.assign(L->n, nullptr);
     L->peer_arena[L->rank] = L->arena;
-    const int64_t Mp = L->Mp, h = L->h, f = L->f, el = L->el;
+    const int64_t Mp = L->Mp, f = L->f, el = L->el;
     TRY_ALLOC(dalloc(&L->w1p, el * 2 * f * h));
     TRY_ALLOC(dalloc(&L->w2, el * h * f));
     TRY_ALLOC(dalloc(&L->wr, L->E * h));
-    TRY_ALLOC(dalloc(&L->ex_loc, L->Tr * L->k));
-    TRY_ALLOC(dalloc(&L->gt_loc, L->Tr * L->k));
-    TRY_ALLOC(dalloc(&L->logits, L->Tr * L->E));
+    TRY_ALLOC(dalloc(&L->ex_loc, Tr * k));
+    TRY_ALLOC(dalloc(&L->gt_loc, Tr * k));
+    TRY_ALLOC(dalloc(&L->logits, Tr * L->E));
     TRY_ALLOC(dalloc(&L->src, L->T));
     TRY_ALLOC(dalloc(&L->dropped, L->T));
-    TRY_ALLOC(dalloc(reinterpret_cast<uint8_t**>(&L->perm_ws), permute_workspace_bytes(L->T, L->E, L->k, L->n)));
-    TRY_ALLOC(dalloc(&L->row_map_in, L->T * L->k));
-    TRY_ALLOC(dalloc(&L->out_expert, L->T * L->k));
-    TRY_ALLOC(dalloc(&L->out_src, L->T * L->k));
+    TRY_ALLOC(dalloc(reinterpret_cast<uint8_t**>(&L->perm_ws), permute_workspace_bytes(L->T, L->E, k, L->n)));
+    TRY_ALLOC(dalloc(&L->row_map_in, L->T * k));
+    TRY_ALLOC(dalloc(&L->out_expert, L->T * k));
+    TRY_ALLOC(dalloc(&L->out_src, L->T * k));
     TRY_ALLOC(dalloc(&L->counts, L->E));
     TRY_ALLOC(dalloc(&L->expert_off, el + 1));
     TRY_ALLOC(dalloc(&L->rows, 1));
@@ -304,27 +317,18 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->dy_perm, Mp * h));
     TRY_ALLOC(dalloc(&L->dfc1, Mp * 2 * f));
     TRY_ALLOC(dalloc(&L->dgate_part, Mp * (f / 256) * 2));
-    TRY_ALLOC(dalloc(&L->dlogits, L->Tr * L->E));
+    TRY_ALLOC(dalloc(&L->dlogits, Tr * L->E));
     TRY_ALLOC(dalloc(&L->ready, Mp / kPad + 1));
-    L->fused_dispatch = getenv("MOE_UNFUSED_DISPATCH") == nullptr;
-    TRY_ALLOC(dalloc(&L->rw_part, ((L->Tr + kRwChunk - 1) / kRwChunk) * L->E * h));
-    TRY_ALLOC(dalloc(&L->t_x, L->n));
-    TRY_ALLOC(dalloc(&L->t_dy, L->n));
-    TRY_ALLOC(dalloc(&L->t_stage, L->n));
-    TRY_ALLOC(dalloc(&L->t_dstage, L->n));
-    TRY_ALLOC(dalloc(&L->t_ex, L->n));
-    TRY_ALLOC(dalloc(&L->t_gt, L->n));
-    TRY_ALLOC(dalloc(&L->t_dgate, L->n));
-    TRY_ALLOC(dalloc(&L->t_flags, L->n));
-    TRY_ALLOC(dalloc(&L->l_x, L->n));
-    TRY_ALLOC(dalloc(&L->l_dy, L->n));
-    TRY_ALLOC(dalloc(&L->l_stage, L->n));
-    TRY_ALLOC(dalloc(&L->l_dstage, L->n));
-    TRY_ALLOC(dalloc(&L->l_dgate, L->n));
+    TRY_ALLOC(dalloc(&L->rw_part, ((Tr + kRwChunk - 1) / kRwChunk) * L->E * h));
+    TRY_ALLOC(dalloc(&L->tab_remote, F_COUNT * L->n));
+    TRY_ALLOC(dalloc(&L->tab_local, F_COUNT * L->n));
     TRY_ALLOC(dalloc(&L->err, 1));
-    cudaMemset(L->err, 0, sizeof(int));
     TRY_ALLOC(dalloc(&L->epoch_dev, 1));
+    cudaMemset(L->err, 0, sizeof(int));
     cudaMemset(L->epoch_dev, 0, sizeof(uint32_t));
+    // the unfused (reference-structure) dispatch path is kept for A/B runs;
+    // gate-after-fc2 backward needs the fused path's row scaling
+    L->fused_dispatch = getenv("MOE_UNFUSED_DISPATCH") == nullptr || L->gate_after || L->fp8;
     // zero the permuted buffers once so never-written rows are finite
     cudaMemset(L->x_perm, 0, Mp * h * 2);
     cudaMemset(L->dy_perm, 0, Mp * h * 2);
@@ -355,8 +359,8 @@ void moe_layer_destroy(moe_layer* L) {
                     L->dropped, L->perm_ws, L->row_map_in, L->out_expert, L->out_src, L->counts,
                     L->expert_off, L->rows, L->gpad_rows, L->gpad_off, L->pad_tok, L->row_dst,
                     L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
-                    L->dgate_part, L->dlogits, L->rw_part, L->ready, L->t_x, L->t_dy, L->t_stage, L->t_dstage, L->t_ex,
-                    L->t_gt, L->t_dgate, L->t_flags, L->l_x, L->l_dy, L->l_stage, L->l_dstage, L->l_dgate, L->err, L->epoch_dev};
+                    L->dgate_part, L->dlogits, L->rw_part, L->ready, L->tab_remote, L->tab_local,
+                    L->err, L->epoch_dev};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
@@ -377,7 +381,7 @@ moe_status moe_layer_set_weights(moe_layer* L, const uint16_t* d_w1, const uint1
     return MOE_OK;
 }
 
-uint16_t* moe_layer_input_buffer(moe_layer* L) { return L ? L->x_sym() : nullptr; }
+uint16_t* moe_layer_input_buffer(moe_layer* L) { return L ? L->mine<uint16_t>(F_X) : nullptr; }
 
 moe_status moe_layer_set_routing(moe_layer* L, const int32_t* d_experts, const float* d_gates,
                                  moe_stream_t stream) {
@@ -397,10 +401,11 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     MOE_CHECK_ARG(L->n == 1 || L->ipc_ready, "ep_size > 1 requires moe_layer_ipc_import");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
+    uint16_t* x_sym = L->mine<uint16_t>(F_X);
     for (int i = 0; i < PH_COUNT; ++i) L->ev_used[i] = false;
     L->mark(PH_ROUTE, s);
-    if (d_x && d_x != L->x_sym())
-        MOE_CUDA_TRY(cudaMemcpyAsync(L->x_sym(), d_x, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
+    if (d_x && d_x != x_sym)
+        MOE_CUDA_TRY(cudaMemcpyAsync(x_sym, d_x, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
     // K1 router (learned mode)
     if (L->cfg.route_mode == 0) {
         const size_t wbytes = (size_t)L->E * h * 2;
@@ -410,33 +415,38 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
                 L->router_attr = true;
             }
-            router_logits_smem_kernel<<<kNumSMs, 512, wbytes, s>>>(L->x_sym(), L->wr, (int)Tr, (int)h,
+            router_logits_smem_kernel<<<kNumSMs, 512, wbytes, s>>>(x_sym, L->wr, (int)Tr, (int)h,
                                                                    (int)L->E, L->logits);
             count_launch();
             MOE_TRY(launch_topk_from_logits(L->logits, Tr, L->E, k, L->ex_loc, L->gt_loc, s));
         } else {
-            MOE_TRY(launch_router_topk(L->x_sym(), L->wr, Tr, h, L->E, k, L->logits, L->ex_loc,
+            MOE_TRY(launch_router_topk(x_sym, L->wr, Tr, h, L->E, k, L->logits, L->ex_loc,
                                        L->gt_loc, s));
         }
     }
+    // FP8 dispatch: quantise this rank's tokens once (per-token E4M3) for the peers to pull
+    if (L->fp8)
+        MOE_TRY(quantize_rows(x_sym, Tr, h, true, L->mine<uint8_t>(F_X8), L->mine<float>(F_XSC), s));
     // routing metadata all-gather over NVLink
     publish_meta_kernel<<<std::min<int64_t>((Tr * k + 255) / 256, 64), 256, 0, s>>>(
-        L->ex_loc, L->gt_loc, (int)(Tr * k), (int)(L->rank * Tr * k), L->t_ex + (L->comm_local ? L->rank : 0),
-        L->t_gt + (L->comm_local ? L->rank : 0), L->comm_local ? 1 : (int)L->n);
+        L->ex_loc, L->gt_loc, (int)(Tr * k), (int)(L->rank * Tr * k),
+        L->tab<int32_t>(F_EX) + (L->comm_local ? L->rank : 0),
+        L->tab<float>(F_GT) + (L->comm_local ? L->rank : 0), L->comm_local ? 1 : (int)L->n);
     count_launch();
     MOE_TRY(barrier(L, 0, s, 1));
     L->mark(PH_PERMUTE, s);
     // K2: capacity drop (replicated on every rank over the global order) + permutation
+    int32_t* ex_all = L->mine<int32_t>(F_EX);
     if (L->cfg.capacity_factor > 0.0)
-        MOE_TRY(launch_capacity_drop(L->ex_all(), L->T, L->E, k, L->n, L->cfg.capacity_factor,
+        MOE_TRY(launch_capacity_drop(ex_all, L->T, L->E, k, L->n, L->cfg.capacity_factor,
                                      L->dropped, s));
     else
         MOE_CUDA_TRY(cudaMemsetAsync(L->dropped, 0, L->T, s));
-    MOE_TRY(launch_permute(L->ex_all(), L->src, L->dropped, L->T, L->E, k, L->n, L->rank, L->n,
+    MOE_TRY(launch_permute(ex_all, L->src, L->dropped, L->T, L->E, k, L->n, L->rank, L->n,
                            L->row_map_in, L->counts, L->out_expert, L->out_src, L->expert_off,
                            L->rows, L->perm_ws, L->gpad_rows, L->gpad_off, L->pad_tok, kPad, s));
     row_info_kernel<<<(unsigned)el, 256, 0, s>>>(L->gpad_off, L->gpad_rows, L->expert_off,
-                                                 L->pad_tok, L->gt_all(), (int)k, (int)Tr,
+                                                 L->pad_tok, L->mine<float>(F_GT), (int)k, (int)Tr,
                                                  L->row_gate, L->row_dst);
     count_launch();
     // dispatch: AG + local scatter (rows pulled from the owning rank)
@@ -444,14 +454,13 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     if (L->fused_dispatch) {
         MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / kPad + 1) * 4, s));
     } else {
-        dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
-                                                         (int)Tr, (int)h, L->tx(), L->x_perm);
+        dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
+                                                         (int)h, L->tab<const uint16_t>(F_X), L->x_perm);
         count_launch();
         MOE_CUDA_TRY(cudaGetLastError());
     }
     // fc1 + SwiGLU (+ gate before fc2)
     L->mark(PH_FC1, s);
-    const bool gate_before = L->cfg.gate_order == MOE_GATE_BEFORE_FC2;
     {
         GemmArgs a{};
         a.G = (int)el;
@@ -463,13 +472,13 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         a.ldo = 2 * f;
         a.out2 = L->fc2_in;
         a.ldo2 = f;
-        a.row_gate = gate_before ? L->row_gate : nullptr;
-        set_dispatch(L, a, L->tx(), L->x_perm);
+        a.row_gate = L->gate_after ? nullptr : L->row_gate;
+        set_dispatch(L, a, false, L->x_perm);
         GemmPlan p = L->p_fc1;
         p.dispatch = L->fused_dispatch;
         MOE_TRY(gemm_launch(p, a, s));
     }
-    // fc2 + gather to the source rank's combine staging
+    // fc2 + gather to the source rank's combine staging (bf16 or FP8 payload)
     L->mark(PH_FC2, s);
     {
         GemmArgs a{};
@@ -480,17 +489,23 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         a.b_group_stride = (int)h;
         a.ldo = h;
         a.row_dst = L->row_dst;
-        a.rank_base = L->tstage();
-        a.row_gate = L->row_gate;
-        a.gate_rows = gate_before ? 0 : 1;
+        a.rank_base = L->fp8 ? L->tab<void>(F_STAGE8) : L->tab<void>(F_STAGE);
+        a.rank_scale_base = L->tab<void>(F_SSC);
         MOE_TRY(gemm_launch(L->p_fc2, a, s));
     }
     MOE_TRY(barrier(L, 1, s, 0));
-    // combine: fixed-order fp32 reduce over the k slots
+    // combine: fixed-order fp32 reduce over the k slots (gate after fc2 applied here)
     L->mark(PH_COMBINE, s);
-    combine_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->stage_sym(), L->dropped + L->rank * Tr,
-                                                      (int)Tr, (int)k, (int)h, d_y, nullptr,
-                                                      nullptr, nullptr, nullptr, nullptr, 0);
+    const uint8_t* drop_loc = L->dropped + L->rank * Tr;
+    const float* slot_gate = L->gate_after ? L->gt_loc : nullptr;
+    if (L->fp8)
+        combine_reduce_kernel<true><<<kNumSMs * 4, 256, 0, s>>>(
+            L->mine<uint8_t>(F_STAGE8), L->mine<float>(F_SSC), drop_loc, (int)Tr, (int)k, (int)h, d_y,
+            slot_gate, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
+    else
+        combine_reduce_kernel<false><<<kNumSMs * 4, 256, 0, s>>>(
+            L->mine<uint16_t>(F_STAGE), nullptr, drop_loc, (int)Tr, (int)k, (int)h, d_y, slot_gate,
+            nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     L->mark(PH_FWD_END, s);
@@ -503,22 +518,38 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
                                  void* dx_ready_event, moe_stream_t stream) {
     MOE_CHECK_ARG(L && d_dy && d_dx, "null argument");
     MOE_CHECK_ARG(L->fwd_done, "backward needs a preceding forward");
-    if (L->cfg.gate_order != MOE_GATE_BEFORE_FC2)
-        return set_error(MOE_ERR_UNSUPPORTED, "backward implemented for gate_order = before_fc2");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
+    uint16_t* dy_sym = L->mine<uint16_t>(F_DY);
+    float* dgate_sym = L->mine<float>(F_DGATE);
+    const uint8_t* drop_loc = L->dropped + L->rank * Tr;
     L->mark(PH_DISPATCH_DY, s);
-    if (d_dy != L->dy_sym())
-        MOE_CUDA_TRY(cudaMemcpyAsync(L->dy_sym(), d_dy, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
-    // dgates of dropped (token, slot)s are never written by an expert rank
-    MOE_CUDA_TRY(cudaMemsetAsync(L->dgate_sym(), 0, Tr * k * 4, s));
+    if (d_dy != dy_sym)
+        MOE_CUDA_TRY(cudaMemcpyAsync(dy_sym, d_dy, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
+    if (L->gate_after) {
+        // dgate on the source rank from the pre-gate outputs still in staging
+        if (L->fp8)
+            dgate_after_kernel<true><<<kNumSMs * 2, 256, 0, s>>>(dy_sym, L->mine<uint8_t>(F_STAGE8),
+                                                                 L->mine<float>(F_SSC), drop_loc,
+                                                                 (int)Tr, (int)k, (int)h, dgate_sym);
+        else
+            dgate_after_kernel<false><<<kNumSMs * 2, 256, 0, s>>>(dy_sym, L->mine<uint16_t>(F_STAGE),
+                                                                  nullptr, drop_loc, (int)Tr, (int)k,
+                                                                  (int)h, dgate_sym);
+        count_launch();
+    } else {
+        // dgates of dropped (token, slot)s are never written by an expert rank
+        MOE_CUDA_TRY(cudaMemsetAsync(dgate_sym, 0, Tr * k * 4, s));
+    }
+    if (L->fp8)
+        MOE_TRY(quantize_rows(dy_sym, Tr, h, false, L->mine<uint8_t>(F_DY8), L->mine<float>(F_DYSC), s));
     MOE_TRY(barrier(L, 2, s, 1));
     // AG(dy) + scatter into permuted order (fused into the fc2 dgrad GEMM)
     if (L->fused_dispatch) {
         MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / kPad + 1) * 4, s));
     } else {
-        dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k,
-                                                         (int)Tr, (int)h, L->tdy(), L->dy_perm);
+        dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
+                                                         (int)h, L->tab<const uint16_t>(F_DY), L->dy_perm);
         count_launch();
     }
     // fc2 dgrad fused with SwiGLU/gate backward and remat of fc2_in
@@ -536,9 +567,9 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.ldo2 = f;
         a.aux = L->fc1_out;
         a.ld_aux = 2 * f;
-        a.row_gate = L->row_gate;
-        a.row_part = L->dgate_part;
-        set_dispatch(L, a, L->tdy(), L->dy_perm);
+        a.row_gate = L->gate_after ? nullptr : L->row_gate;
+        a.row_part = L->gate_after ? nullptr : L->dgate_part;
+        set_dispatch(L, a, true, L->dy_perm);
         GemmPlan p = L->p_fc2_dgrad;
         p.dispatch = L->fused_dispatch;
         MOE_TRY(gemm_launch(p, a, s));
@@ -554,21 +585,30 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.b_group_stride = (int)(2 * f);
         a.ldo = h;
         a.row_dst = L->row_dst;
-        a.rank_base = L->tdstage();
+        a.rank_base = L->fp8 ? L->tab<void>(F_DSTAGE8) : L->tab<void>(F_DSTAGE);
+        a.rank_scale_base = L->tab<void>(F_DSSC);
         MOE_TRY(gemm_launch(L->p_fc1_dgrad, a, s));
     }
     L->mark(PH_DGATE, s);
-    dgate_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgate_part, (int)(f / 256) * 2, L->row_dst,
-                                                L->gpad_off + el, L->tdgate());
-    count_launch();
+    if (!L->gate_after) {
+        dgate_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgate_part, (int)(f / 256) * 2, L->row_dst,
+                                                    L->gpad_off + el, L->tab<float>(F_DGATE));
+        count_launch();
+    }
     MOE_TRY(barrier(L, 3, s, 0));
     L->mark(PH_COMBINE_DX, s);
     const bool router = L->cfg.route_mode == 0;
-    combine_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(
-        L->dstage_sym(), L->dropped + L->rank * Tr, (int)Tr, (int)k, (int)h, d_dx,
-        router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
-        router ? L->dgate_sym() : nullptr, router ? L->wr : nullptr,
-        router ? L->dlogits : nullptr, (int)L->E);
+    if (L->fp8)
+        combine_reduce_kernel<true><<<kNumSMs * 4, 256, 0, s>>>(
+            L->mine<uint8_t>(F_DSTAGE8), L->mine<float>(F_DSSC), drop_loc, (int)Tr, (int)k, (int)h,
+            d_dx, nullptr, router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
+            router ? dgate_sym : nullptr, router ? L->wr : nullptr, router ? L->dlogits : nullptr,
+            (int)L->E);
+    else
+        combine_reduce_kernel<false><<<kNumSMs * 4, 256, 0, s>>>(
+            L->mine<uint16_t>(F_DSTAGE), nullptr, drop_loc, (int)Tr, (int)k, (int)h, d_dx, nullptr,
+            router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr, router ? dgate_sym : nullptr,
+            router ? L->wr : nullptr, router ? L->dlogits : nullptr, (int)L->E);
     count_launch();
     // dx is final here: callers may start its device->host copy while the
     // weight gradients below run (wgrad hidden under the dx transfer)
@@ -602,10 +642,10 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
             const int nch = (int)((Tr + kRwChunk - 1) / kRwChunk);
             if (L->E <= 8)
                 router_wgrad_partial_kernel<8><<<dim3((unsigned)((h + 255) / 256), nch), 256, 0, s>>>(
-                    L->dlogits, L->x_sym(), (int)Tr, (int)h, (int)L->E, L->rw_part);
+                    L->dlogits, L->mine<uint16_t>(F_X), (int)Tr, (int)h, (int)L->E, L->rw_part);
             else
                 router_wgrad_partial_kernel<32><<<dim3((unsigned)((h + 255) / 256), nch), 256, 0, s>>>(
-                    L->dlogits, L->x_sym(), (int)Tr, (int)h, (int)L->E, L->rw_part);
+                    L->dlogits, L->mine<uint16_t>(F_X), (int)Tr, (int)h, (int)L->E, L->rw_part);
             router_wgrad_reduce_kernel<<<kNumSMs * 2, 256, 0, s>>>(L->rw_part, nch, (int)L->E,
                                                                    (int)h, d_dwr);
             count_launch(2);
@@ -625,15 +665,15 @@ moe_status moe_layer_backward(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx
 
 moe_status moe_layer_routing(moe_layer* L, moe_layer_routing_view* v) {
     MOE_CHECK_ARG(L && v, "null argument");
-    v->experts = L->ex_all();
-    v->gates = L->gt_all();
+    v->experts = L->mine<int32_t>(F_EX);
+    v->gates = L->mine<float>(F_GT);
     v->dropped = L->dropped;
     v->row_map_in = L->row_map_in;
     v->per_expert_counts = L->counts;
     v->out_expert = L->out_expert;
     v->out_source_rank = L->out_src;
     v->rows = L->rows;
-    v->dgates = L->dgate_sym();
+    v->dgates = L->mine<float>(F_DGATE);
     v->logits = L->logits;
     return MOE_OK;
 }

@@ -48,6 +48,7 @@ __global__ void dispatch_rows_kernel(const int32_t* __restrict__ pad_row_tok, co
                                      int k, int tokens_per_rank, int h,
                                      const uint16_t* const* __restrict__ src_bufs,
                                      uint16_t* __restrict__ dst) {
+    // (unfused reference path: bf16 only, no row scaling)
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -82,27 +83,33 @@ __device__ __forceinline__ void softmax_topk_bwd(const float* g, const float* dg
 
 // Combine: y[t, :] = sum over slots (fixed slot order, fp32) of the staged
 // expert outputs (a2a_fp32 semantics, numerics.cpp:172-192); dropped tokens
-// produce 0. Optional router term for dx: += sum_j dlogit_j * wr[e_j, :].
-// One warp per token; each lane owns 8-column groups.
-__global__ void combine_reduce_kernel(const uint16_t* __restrict__ stage, const uint8_t* __restrict__ dropped,
-                                      int T, int k, int h, uint16_t* __restrict__ out,
+// produce 0. FP8 = staged rows are grouped-128 E4M3 codes + fp32 scales
+// (dequantised on arrival). slot_gate (gate after fc2, numerics.hpp:84-86)
+// multiplies each slot. Optional router term for dx:
+// += sum_j dlogit_j * wr[e_j, :]. One warp per token; lanes own 16 columns.
+template <bool FP8>
+__global__ void combine_reduce_kernel(const void* __restrict__ stage_v, const float* __restrict__ stage_scale,
+                                      const uint8_t* __restrict__ dropped, int T, int k, int h,
+                                      uint16_t* __restrict__ out, const float* __restrict__ slot_gate,
                                       const int32_t* __restrict__ experts, const float* __restrict__ gates,
                                       const float* __restrict__ dgates, const uint16_t* __restrict__ wr,
                                       float* __restrict__ dlogits, int E) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int nvec = h / 8;
+    const int nv16 = h / 16;
     for (int t = warp; t < T; t += nwarps) {
         uint4* o = reinterpret_cast<uint4*>(out + (int64_t)t * h);
         if (dropped && dropped[t]) {
-            for (int v = lane; v < nvec; v += 32) o[v] = make_uint4(0, 0, 0, 0);
-            if (dlogits && lane < E) for (int e = lane; e < E; e += 32) dlogits[(int64_t)t * E + e] = 0.0f;
+            for (int v = lane; v < h / 8; v += 32) o[v] = make_uint4(0, 0, 0, 0);
+            if (dlogits) for (int e = lane; e < E; e += 32) dlogits[(int64_t)t * E + e] = 0.0f;
             continue;
         }
         float dl[8];
         int ex[8];
+        float sg[8];
         const bool router = wr != nullptr;
+        for (int j = 0; j < k; ++j) sg[j] = slot_gate ? slot_gate[(int64_t)t * k + j] : 1.0f;
         if (router) {
             float g[8], dg[8];
             for (int j = 0; j < k; ++j) {
@@ -119,26 +126,183 @@ __global__ void combine_reduce_kernel(const uint16_t* __restrict__ stage, const 
                 }
             }
         }
-        for (int v = lane; v < nvec; v += 32) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int v = lane; v < nv16; v += 32) {
+            float acc[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] = 0.0f;
             for (int j = 0; j < k; ++j) {
-                const uint4 sv = reinterpret_cast<const uint4*>(stage + ((int64_t)t * k + j) * h)[v];
-                const float2 p0 = unpack_bf16x2(sv.x), p1 = unpack_bf16x2(sv.y),
-                             p2 = unpack_bf16x2(sv.z), p3 = unpack_bf16x2(sv.w);
-                acc[0] += p0.x; acc[1] += p0.y; acc[2] += p1.x; acc[3] += p1.y;
-                acc[4] += p2.x; acc[5] += p2.y; acc[6] += p3.x; acc[7] += p3.y;
+                const int64_t row = (int64_t)t * k + j;
+                if (FP8) {
+                    const uint4 c = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(stage_v) + row * h)[v];
+                    const float f = stage_scale[row * (h / 128) + (v * 16) / 128] * sg[j];
+                    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 lo = e4m3x2_to_f32x2((uint16_t)(w[q] & 0xffff));
+                        const float2 hi = e4m3x2_to_f32x2((uint16_t)(w[q] >> 16));
+                        acc[4 * q] += lo.x * f; acc[4 * q + 1] += lo.y * f;
+                        acc[4 * q + 2] += hi.x * f; acc[4 * q + 3] += hi.y * f;
+                    }
+                } else {
+                    const uint4* sp = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(stage_v) + row * h);
+                    const uint4 s0 = sp[2 * v], s1 = sp[2 * v + 1];
+                    const uint32_t w[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float2 p = unpack_bf16x2(w[q]);
+                        acc[2 * q] += p.x * sg[j];
+                        acc[2 * q + 1] += p.y * sg[j];
+                    }
+                }
             }
             if (router) {
                 for (int j = 0; j < k; ++j) {
-                    const uint4 wv = reinterpret_cast<const uint4*>(wr + (int64_t)ex[j] * h)[v];
-                    const float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y),
-                                 w2 = unpack_bf16x2(wv.z), w3 = unpack_bf16x2(wv.w);
-                    acc[0] += dl[j] * w0.x; acc[1] += dl[j] * w0.y; acc[2] += dl[j] * w1.x; acc[3] += dl[j] * w1.y;
-                    acc[4] += dl[j] * w2.x; acc[5] += dl[j] * w2.y; acc[6] += dl[j] * w3.x; acc[7] += dl[j] * w3.y;
+                    const uint4* wp = reinterpret_cast<const uint4*>(wr + (int64_t)ex[j] * h);
+                    const uint4 w0 = wp[2 * v], w1 = wp[2 * v + 1];
+                    const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float2 p = unpack_bf16x2(w[q]);
+                        acc[2 * q] += dl[j] * p.x;
+                        acc[2 * q + 1] += dl[j] * p.y;
+                    }
                 }
             }
-            o[v] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                              pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+            o[2 * v] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                                  pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+            o[2 * v + 1] = make_uint4(pack_bf16x2(acc[8], acc[9]), pack_bf16x2(acc[10], acc[11]),
+                                      pack_bf16x2(acc[12], acc[13]), pack_bf16x2(acc[14], acc[15]));
+        }
+    }
+}
+
+// Gate-after-fc2 backward on the source rank (numerics.hpp:84-86):
+// dgate[t, j] = <dy[t, :], fc2_out[t, j, :]> with fc2_out the pre-gate expert
+// output still held in this rank's combine staging from the forward pass.
+template <bool FP8>
+__global__ void dgate_after_kernel(const uint16_t* __restrict__ dy, const void* __restrict__ stage_v,
+                                   const float* __restrict__ stage_scale, const uint8_t* __restrict__ dropped,
+                                   int T, int k, int h, float* __restrict__ dgate) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int t = warp; t < T; t += nwarps) {
+        const bool drop = dropped && dropped[t];
+        for (int j = 0; j < k; ++j) {
+            const int64_t row = (int64_t)t * k + j;
+            float acc = 0.0f;
+            if (!drop) {
+                for (int v = lane; v < h / 16; v += 32) {
+                    const uint4* dp = reinterpret_cast<const uint4*>(dy + (int64_t)t * h);
+                    const uint4 d0 = dp[2 * v], d1 = dp[2 * v + 1];
+                    const uint32_t dw[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+                    float sv[16];
+                    if (FP8) {
+                        const uint4 c = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(stage_v) + row * h)[v];
+                        const float f = stage_scale[row * (h / 128) + (v * 16) / 128];
+                        const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float2 lo = e4m3x2_to_f32x2((uint16_t)(w[q] & 0xffff));
+                            const float2 hi = e4m3x2_to_f32x2((uint16_t)(w[q] >> 16));
+                            sv[4 * q] = lo.x * f; sv[4 * q + 1] = lo.y * f;
+                            sv[4 * q + 2] = hi.x * f; sv[4 * q + 3] = hi.y * f;
+                        }
+                    } else {
+                        const uint4* sp = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(stage_v) + row * h);
+                        const uint4 s0 = sp[2 * v], s1 = sp[2 * v + 1];
+                        const uint32_t w[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float2 p = unpack_bf16x2(w[q]);
+                            sv[2 * q] = p.x;
+                            sv[2 * q + 1] = p.y;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float2 d = unpack_bf16x2(dw[q]);
+                        acc += d.x * sv[2 * q] + d.y * sv[2 * q + 1];
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            }
+            if (lane == 0) dgate[row] = drop ? 0.0f : acc;
+        }
+    }
+}
+
+// Source-side E4M3 quantisation of this rank's rows before they are pulled
+// over NVLink (FP8 communication): GROUP = 0 -> one scale
+// per row (per_token, forward), else one per GROUP columns (grouped-128,
+// backward). fp32 arithmetic, RNE + saturation at 448.
+template <int GROUP>
+__global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int rows, int cols,
+                                     uint8_t* __restrict__ codes, float* __restrict__ scales) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < rows; r += nwarps) {
+        const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)r * cols);
+        if (GROUP == 0) {
+            float m = 0.0f;
+            for (int v = lane; v < cols / 8; v += 32) {
+                const uint4 a = xr[v];
+                const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 p = unpack_bf16x2(w[q]);
+                    m = fmaxf(m, fmaxf(fabsf(p.x), fabsf(p.y)));
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+            const float scale = m > 0.0f ? m / 448.0f : 1.0f;
+            const float inv = 1.0f / scale;
+            if (lane == 0) scales[r] = scale;
+            for (int v = lane; v < cols / 8; v += 32) {
+                const uint4 a = xr[v];
+                const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+                uint32_t pk[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const float2 p0 = unpack_bf16x2(w[2 * q]), p1 = unpack_bf16x2(w[2 * q + 1]);
+                    pk[q] = (uint32_t)f32x2_to_e4m3x2(p0.x * inv, p0.y * inv) |
+                            ((uint32_t)f32x2_to_e4m3x2(p1.x * inv, p1.y * inv) << 16);
+                }
+                *reinterpret_cast<uint2*>(codes + (int64_t)r * cols + v * 8) = make_uint2(pk[0], pk[1]);
+            }
+        } else {
+            // GROUP/8 lanes per group; lanes exchange within their group
+            constexpr int LPG = GROUP / 8;
+            for (int v0 = 0; v0 < cols / 8; v0 += 32) {
+                const int v = v0 + lane;
+                uint4 a = make_uint4(0, 0, 0, 0);
+                if (v < cols / 8) a = xr[v];
+                const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+                float m = 0.0f;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 p = unpack_bf16x2(w[q]);
+                    m = fmaxf(m, fmaxf(fabsf(p.x), fabsf(p.y)));
+                }
+#pragma unroll
+                for (int off = LPG / 2; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+                const float scale = m > 0.0f ? m / 448.0f : 1.0f;
+                const float inv = 1.0f / scale;
+                if (v < cols / 8) {
+                    if ((lane % LPG) == 0) scales[(int64_t)r * (cols / GROUP) + (v * 8) / GROUP] = scale;
+                    uint32_t pk[2];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const float2 p0 = unpack_bf16x2(w[2 * q]), p1 = unpack_bf16x2(w[2 * q + 1]);
+                        pk[q] = (uint32_t)f32x2_to_e4m3x2(p0.x * inv, p0.y * inv) |
+                                ((uint32_t)f32x2_to_e4m3x2(p1.x * inv, p1.y * inv) << 16);
+                    }
+                    *reinterpret_cast<uint2*>(codes + (int64_t)r * cols + v * 8) = make_uint2(pk[0], pk[1]);
+                }
+            }
         }
     }
 }

@@ -19,14 +19,16 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def make_layer(T, h, f, E, k, seed=0, route_mode="learned", cf=0.0):
+def make_layer(T, h, f, E, k, seed=0, route_mode="learned", cf=0.0, gate_order="before_fc2_in",
+               comm_format="bf16"):
     from paper_2505_11432_b200.layer import MoELayer
     g = torch.Generator().manual_seed(seed)
     x = (torch.randn(T, h, generator=g) * 0.5).bfloat16()
     w1 = (torch.randn(E, 2 * f, h, generator=g) / h ** 0.5).bfloat16()
     w2 = (torch.randn(E, h, f, generator=g) / f ** 0.5).bfloat16()
     wr = (torch.randn(E, h, generator=g) / h ** 0.5).bfloat16()
-    L = MoELayer(T, h, f, E, k, capacity_factor=cf, route_mode=route_mode)
+    L = MoELayer(T, h, f, E, k, capacity_factor=cf, route_mode=route_mode, gate_order=gate_order,
+                 comm_format=comm_format)
     L.set_weights(w1.cuda(), w2.cuda(), wr.cuda())
     return L, x, w1, w2, wr
 
@@ -96,3 +98,34 @@ def test_layer_injected_routing_with_drops():
     assert rel(dw1.float().cpu().numpy(), ob["dw1"]) < TOL
     assert rel(dw2.float().cpu().numpy(), ob["dw2"]) < TOL
     assert rel(L.routing()["dgates"].cpu().numpy(), ob["dgates"]) < TOL
+
+
+# FP8 communication (E4M3 per-token dispatch, grouped-128 combine / backward
+# exchanges): stated tolerance 5e-2 relative L2 against the fp32 oracle.
+TOL_FP8 = 5e-2
+
+
+@pytest.mark.parametrize("gate_order,comm,tol", [("after_fc2_out", "bf16", TOL),
+                                                  ("before_fc2_in", "fp8", TOL_FP8),
+                                                  ("after_fc2_out", "fp8", TOL_FP8)])
+def test_layer_gate_order_and_fp8_comm(gate_order, comm, tol):
+    import pyoracle as P
+    T, h, f, E, k = 256, 512, 512, 8, 2
+    L, x, w1, w2, wr = make_layer(T, h, f, E, k, seed=5, gate_order=gate_order, comm_format=comm)
+    y = L.forward(x.cuda())
+    torch.cuda.synchronize()
+    r = L.routing()
+    ex, gt, dr, lg = (r[q].cpu().numpy() for q in ("experts", "gates", "dropped", "logits"))
+    xf, w1f, w2f, wrf = (t.float().numpy() for t in (x, w1, w2, wr))
+    ga = gate_order.startswith("after")
+    oy = P.orc_moe_forward(xf, ex, gt, dr, w1f, w2f, gate_after=ga)
+    assert rel(y.float().cpu().numpy(), oy) < tol
+    dy = (torch.randn(T, h, generator=torch.Generator().manual_seed(9)) * 0.1).bfloat16()
+    dx, dw1, dw2, dwr = L.backward(dy.cuda())
+    torch.cuda.synchronize()
+    ob = P.orc_moe_backward(xf, dy.float().numpy(), ex, gt, lg, dr, w1f, w2f, wrf, gate_after=ga)
+    errs = dict(dgates=rel(L.routing()["dgates"].cpu().numpy(), ob["dgates"]),
+                dx=rel(dx.float().cpu().numpy(), ob["dx"]), dw1=rel(dw1.float().cpu().numpy(), ob["dw1"]),
+                dw2=rel(dw2.float().cpu().numpy(), ob["dw2"]), dwr=rel(dwr.cpu().numpy(), ob["dwr"]))
+    print(gate_order, comm, errs)
+    assert all(v < tol for v in errs.values()), errs

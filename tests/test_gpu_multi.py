@@ -27,6 +27,12 @@ def test_ep2_layer_parity(cf):
     _run(2, {"MP_CF": cf})
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("gate,comm", [("after_fc2_out", "fp8"), ("before_fc2_in", "fp8"), ("after_fc2_out", "bf16")])
+def test_ep2_gate_order_fp8(gate, comm):
+    _run(2, {"MP_CF": "1.0", "MP_GATE": gate, "MP_COMM": comm})
+
+
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
 def test_ep4_layer_parity():
     _run(4, {"MP_CF": "1.25"})
