@@ -73,6 +73,8 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s) {
     // single-CTA versions
     MOE_GEMM_CASE(256, 1, false, false, false, EPI_SWIGLU)
     MOE_GEMM_CASE(256, 1, false, false, false, EPI_SCATTER)
+    MOE_GEMM_CASE(256, 1, false, false, false, EPI_SCATTER_FP8)
+    MOE_GEMM_CASE(256, 1, false, true, false, EPI_SCATTER_FP8)
     MOE_GEMM_CASE(256, 1, false, true, false, EPI_SWIGLU_BWD)
     MOE_GEMM_CASE(256, 1, false, true, false, EPI_SCATTER)
     MOE_GEMM_CASE(256, 1, true, true, true, EPI_STORE_BF16)

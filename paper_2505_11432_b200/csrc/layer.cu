@@ -27,8 +27,6 @@ namespace moe {
 
 namespace {
 size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
-constexpr int kCG = 2;          // CTA-pair GEMMs
-constexpr int kPad = 128 * kCG;  // expert row segments padded to the tile height
 
 // fields of the symmetric arena (same offsets on every rank)
 enum Field {
@@ -53,6 +51,13 @@ struct moe_layer {
     int64_t Tr = 0, T = 0, h = 0, f = 0, E = 0, k = 0, n = 1, rank = 0, el = 0, first = 0, Mp = 0;
     int dev = 0;
     bool fp8 = false, gate_after = false;
+    // GEMM tiling: cg = 2 -> CTA-pair 256-row tiles (expert segments padded to
+    // 256 rows); cg = 1 -> 128-row tiles for fine-grained experts where the
+    // padding would cost more than the pair gains
+    int cg = 2, pad = 256;
+    bool gemm_router = false;  // router logits on the tensor cores (large E*h)
+    int32_t* router_rows = nullptr;
+    moe::GemmPlan p_router;
     // symmetric arena (IPC-exported)
     uint8_t* arena = nullptr;
     size_t arena_bytes = 0;
@@ -77,7 +82,7 @@ struct moe_layer {
     uint16_t *x_perm = nullptr, *fc1_out = nullptr, *fc2_in = nullptr, *dy_perm = nullptr,
              *dfc1 = nullptr;
     float *dgate_part = nullptr, *dlogits = nullptr, *rw_part = nullptr;
-    uint32_t* ready = nullptr;  // fused-dispatch arrival counters [Mp / kPad]
+    uint32_t* ready = nullptr;  // fused-dispatch arrival counters [Mp / L->pad]
     bool fused_dispatch = true;
     int* err = nullptr;
     uint32_t* epoch_dev = nullptr;
@@ -134,12 +139,12 @@ moe_status build_plans(moe_layer* L) {
     L->p_fc1 = GemmPlan{};
     L->p_fc1.epi = EPI_SWIGLU;
     MOE_TRY(tmap_kmajor(&L->p_fc1.ta, L->x_perm, Mp, h, 128));
-    MOE_TRY(tmap_kmajor(&L->p_fc1.tb, L->w1p, el * 2 * f, h, 256 / kCG));
+    MOE_TRY(tmap_kmajor(&L->p_fc1.tb, L->w1p, el * 2 * f, h, 256 / L->cg));
     // forward fc2: A = fc2_in [Mp, f], B = w2 [el*h, f] (K-major)
     L->p_fc2 = GemmPlan{};
     L->p_fc2.epi = L->fp8 ? EPI_SCATTER_FP8 : EPI_SCATTER;
     MOE_TRY(tmap_kmajor(&L->p_fc2.ta, L->fc2_in, Mp, f, 128));
-    MOE_TRY(tmap_kmajor(&L->p_fc2.tb, L->w2, el * h, f, 256 / kCG));
+    MOE_TRY(tmap_kmajor(&L->p_fc2.tb, L->w2, el * h, f, 256 / L->cg));
     // fc2 dgrad: A = dy_perm [Mp, h], B(n=f, k=h) = w2[e][k][n] (MN-major)
     L->p_fc2_dgrad = GemmPlan{};
     L->p_fc2_dgrad.epi = EPI_SWIGLU_BWD;
@@ -166,7 +171,19 @@ moe_status build_plans(moe_layer* L) {
     MOE_TRY(tmap_mnmajor(&L->p_fc1_wgrad.tb, L->x_perm, Mp, h));
     for (GemmPlan* p : {&L->p_fc1, &L->p_fc2, &L->p_fc2_dgrad, &L->p_fc2_wgrad, &L->p_fc1_dgrad,
                         &L->p_fc1_wgrad})
-        p->cg = kCG;
+        p->cg = L->cg;
+    // router logits[T_r, E] = x . wr^T on the tensor cores when W_r does not
+    // fit in shared memory (DeepSeek shape: E = 256, h = 7168)
+    L->gemm_router = (size_t)L->E * h * 2 > 200 * 1024 || L->E > 64;
+    if (L->gemm_router) {
+        L->p_router = GemmPlan{};
+        L->p_router.epi = EPI_STORE_F32;
+        L->p_router.cg = (L->Tr % 256 == 0) ? 2 : 1;
+        MOE_TRY(tmap_kmajor(&L->p_router.ta, L->arena + L->off[F_X], L->Tr, h, 128));
+        MOE_TRY(tmap_kmajor(&L->p_router.tb, L->wr, L->E, h, 256 / L->p_router.cg));
+        const int32_t rr = (int32_t)L->Tr;
+        MOE_CUDA_TRY(cudaMemcpy(L->router_rows, &rr, sizeof(rr), cudaMemcpyHostToDevice));
+    }
     return MOE_OK;
 }
 
@@ -255,7 +272,14 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     L->k = c.top_k;
     L->el = L->E / L->n;
     L->first = L->rank * L->el;
-    L->Mp = L->T * L->k + L->el * kPad;
+    {
+        // ~12% per-FLOP gain of CTA pairs vs. 64 rows of average extra padding per expert
+        const double rows_per_expert = double(L->T * L->k) / double(L->E);
+        L->cg = rows_per_expert >= 512.0 ? 2 : 1;
+        if (const char* e = getenv("MOE_GEMM_CG")) L->cg = atoi(e) == 1 ? 1 : 2;
+        L->pad = 128 * L->cg;
+    }
+    L->Mp = L->T * L->k + L->el * L->pad;
     MOE_CHECK_ARG(L->T * L->k < (1ll << 27), "T*k must be < 2^27");
     cudaGetDevice(&L->dev);
 
@@ -318,12 +342,13 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->dfc1, Mp * 2 * f));
     TRY_ALLOC(dalloc(&L->dgate_part, Mp * (f / 256) * 2));
     TRY_ALLOC(dalloc(&L->dlogits, Tr * L->E));
-    TRY_ALLOC(dalloc(&L->ready, Mp / kPad + 1));
+    TRY_ALLOC(dalloc(&L->ready, Mp / L->pad + 1));
     TRY_ALLOC(dalloc(&L->rw_part, ((Tr + kRwChunk - 1) / kRwChunk) * L->E * h));
     TRY_ALLOC(dalloc(&L->tab_remote, F_COUNT * L->n));
     TRY_ALLOC(dalloc(&L->tab_local, F_COUNT * L->n));
     TRY_ALLOC(dalloc(&L->err, 1));
     TRY_ALLOC(dalloc(&L->epoch_dev, 1));
+    TRY_ALLOC(dalloc(&L->router_rows, 1));
     cudaMemset(L->err, 0, sizeof(int));
     cudaMemset(L->epoch_dev, 0, sizeof(uint32_t));
     // the unfused (reference-structure) dispatch path is kept for A/B runs;
@@ -360,7 +385,7 @@ void moe_layer_destroy(moe_layer* L) {
                     L->expert_off, L->rows, L->gpad_rows, L->gpad_off, L->pad_tok, L->row_dst,
                     L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
                     L->dgate_part, L->dlogits, L->rw_part, L->ready, L->tab_remote, L->tab_local,
-                    L->err, L->epoch_dev};
+                    L->err, L->epoch_dev, L->router_rows};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
@@ -409,7 +434,18 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     // K1 router (learned mode)
     if (L->cfg.route_mode == 0) {
         const size_t wbytes = (size_t)L->E * h * 2;
-        if (wbytes <= 200 * 1024) {
+        if (L->gemm_router) {
+            GemmArgs a{};
+            a.G = 1;
+            a.group_rows = L->router_rows;
+            a.N = (int)L->E;
+            a.K = (int)h;
+            a.b_group_stride = 0;
+            a.out = L->logits;
+            a.ldo = L->E;
+            MOE_TRY(gemm_launch(L->p_router, a, s));
+            MOE_TRY(launch_topk_from_logits(L->logits, Tr, L->E, k, L->ex_loc, L->gt_loc, s));
+        } else if (wbytes <= 200 * 1024) {
             if (!L->router_attr) {
                 MOE_CUDA_TRY(cudaFuncSetAttribute(router_logits_smem_kernel,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -444,7 +480,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         MOE_CUDA_TRY(cudaMemsetAsync(L->dropped, 0, L->T, s));
     MOE_TRY(launch_permute(ex_all, L->src, L->dropped, L->T, L->E, k, L->n, L->rank, L->n,
                            L->row_map_in, L->counts, L->out_expert, L->out_src, L->expert_off,
-                           L->rows, L->perm_ws, L->gpad_rows, L->gpad_off, L->pad_tok, kPad, s));
+                           L->rows, L->perm_ws, L->gpad_rows, L->gpad_off, L->pad_tok, L->pad, s));
     row_info_kernel<<<(unsigned)el, 256, 0, s>>>(L->gpad_off, L->gpad_rows, L->expert_off,
                                                  L->pad_tok, L->mine<float>(F_GT), (int)k, (int)Tr,
                                                  L->row_gate, L->row_dst);
@@ -452,7 +488,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     // dispatch: AG + local scatter (rows pulled from the owning rank)
     L->mark(PH_DISPATCH, s);
     if (L->fused_dispatch) {
-        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / kPad + 1) * 4, s));
+        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 1) * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
                                                          (int)h, L->tab<const uint16_t>(F_X), L->x_perm);
@@ -546,7 +582,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     MOE_TRY(barrier(L, 2, s, 1));
     // AG(dy) + scatter into permuted order (fused into the fc2 dgrad GEMM)
     if (L->fused_dispatch) {
-        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / kPad + 1) * 4, s));
+        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 1) * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
                                                          (int)h, L->tab<const uint16_t>(F_DY), L->dy_perm);
