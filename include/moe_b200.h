@@ -251,6 +251,38 @@ moe_status moe_layer_ipc_export(moe_layer* L, void* h_blob);
  * order) and map peer buffers. Call once after every rank exported. */
 moe_status moe_layer_ipc_import(moe_layer* L, const void* h_blobs);
 
+/* ===================================================================== */
+/* Sequence-parallel attention projections (TP weights, SP activations)   */
+/* reference nodes ag_attn_in + qkv_proj, out_proj + rs_attn_out,          */
+/* graph.cpp:202-214; cost formulas commcost.cpp:61-64                     */
+/* ===================================================================== */
+
+typedef struct moe_attn moe_attn; /* opaque */
+
+/* seq = full sequence length s (sharded s/tp per rank), qkv_cols_per_rank =
+ * h (1 + 2/m) / tp for GQA ratio m (graph.cpp:163-165). */
+moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_rank,
+                           int64_t tp_size, int64_t rank, moe_attn** out);
+void moe_attn_destroy(moe_attn* A);
+/* This rank's symmetric [s/tp, h] input shard buffer. */
+uint16_t* moe_attn_input_buffer(moe_attn* A);
+/* wqkv [qkv_cols_per_rank, h] (K-major, nn.Linear layout); wout [h, h/tp]. */
+moe_status moe_attn_set_weights(moe_attn* A, const uint16_t* d_wqkv, const uint16_t* d_wout,
+                                moe_stream_t stream);
+/* AG-GEMM: qkv[s, qkv_cols] = AllGather_seq(x_shard) . wqkv^T, the gather
+ * fused into the GEMM (in-kernel NVLink pulls gated per 256-row block).
+ * d_x_shard may be NULL if the shard was written into the input buffer. */
+moe_status moe_attn_ag_gemm(moe_attn* A, const uint16_t* d_x_shard, uint16_t* d_qkv,
+                            moe_stream_t stream);
+/* GEMM-RS: y_shard[s/tp, h] = sum over ranks of (o[s, h/tp] . wout^T), rows
+ * pushed to their owner from the GEMM epilogue, fixed-order fp32 reduce. */
+moe_status moe_attn_gemm_rs(moe_attn* A, const uint16_t* d_o, uint16_t* d_y_shard,
+                            moe_stream_t stream);
+size_t moe_attn_ipc_handle_size(void);
+moe_status moe_attn_ipc_export(moe_attn* A, void* h_blob);
+moe_status moe_attn_ipc_import(moe_attn* A, const void* h_blobs);
+int moe_attn_error_flag(moe_attn* A);
+
 #ifdef __cplusplus
 }
 #endif

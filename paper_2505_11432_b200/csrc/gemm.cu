@@ -57,6 +57,8 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s) {
     MOE_GEMM_CASE_DISP(256, 2, false, true, false, EPI_SWIGLU_BWD)
     MOE_GEMM_CASE_DISP(256, 1, false, false, false, EPI_SWIGLU)
     MOE_GEMM_CASE_DISP(256, 1, false, true, false, EPI_SWIGLU_BWD)
+    MOE_GEMM_CASE_DISP(256, 2, false, false, false, EPI_STORE_BF16)  // attention AG-GEMM
+    MOE_GEMM_CASE_DISP(256, 1, false, false, false, EPI_STORE_BF16)
     // layer GEMMs, CTA-pair (cta_group::2) versions
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_SWIGLU)       // fc1 + SwiGLU
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_SCATTER)      // fc2 + gather

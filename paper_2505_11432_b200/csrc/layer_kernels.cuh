@@ -15,7 +15,7 @@ namespace moe {
 
 // Per padded permuted row: source token-slot, gate, combine destination.
 // Grid: one block per local expert.
-__global__ void row_info_kernel(const int32_t* __restrict__ group_pad_off,
+static __global__ void row_info_kernel(const int32_t* __restrict__ group_pad_off,
                                 const int32_t* __restrict__ group_pad_rows,
                                 const int32_t* __restrict__ expert_offsets,
                                 int32_t* __restrict__ pad_row_tok,  // in: real rows; out: -1 pads
@@ -44,7 +44,7 @@ __global__ void row_info_kernel(const int32_t* __restrict__ group_pad_off,
 // pads (AG + local scatter fused: rows are pulled straight from the owning
 // rank's buffer over NVLink into permuted order).
 // One warp per row, 16-byte vectors, 4 in flight per lane.
-__global__ void dispatch_rows_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad,
+static __global__ void dispatch_rows_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad,
                                      int k, int tokens_per_rank, int h,
                                      const uint16_t* const* __restrict__ src_bufs,
                                      uint16_t* __restrict__ dst) {
@@ -88,7 +88,7 @@ __device__ __forceinline__ void softmax_topk_bwd(const float* g, const float* dg
 // multiplies each slot. Optional router term for dx:
 // += sum_j dlogit_j * wr[e_j, :]. One warp per token; lanes own 16 columns.
 template <bool FP8>
-__global__ void combine_reduce_kernel(const void* __restrict__ stage_v, const float* __restrict__ stage_scale,
+static __global__ void combine_reduce_kernel(const void* __restrict__ stage_v, const float* __restrict__ stage_scale,
                                       const uint8_t* __restrict__ dropped, int T, int k, int h,
                                       uint16_t* __restrict__ out, const float* __restrict__ slot_gate,
                                       const int32_t* __restrict__ experts, const float* __restrict__ gates,
@@ -180,7 +180,7 @@ __global__ void combine_reduce_kernel(const void* __restrict__ stage_v, const fl
 // dgate[t, j] = <dy[t, :], fc2_out[t, j, :]> with fc2_out the pre-gate expert
 // output still held in this rank's combine staging from the forward pass.
 template <bool FP8>
-__global__ void dgate_after_kernel(const uint16_t* __restrict__ dy, const void* __restrict__ stage_v,
+static __global__ void dgate_after_kernel(const uint16_t* __restrict__ dy, const void* __restrict__ stage_v,
                                    const float* __restrict__ stage_scale, const uint8_t* __restrict__ dropped,
                                    int T, int k, int h, float* __restrict__ dgate) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -238,7 +238,7 @@ __global__ void dgate_after_kernel(const uint16_t* __restrict__ dy, const void* 
 // per row (per_token, forward), else one per GROUP columns (grouped-128,
 // backward). fp32 arithmetic, RNE + saturation at 448.
 template <int GROUP>
-__global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int rows, int cols,
+static __global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int rows, int cols,
                                      uint8_t* __restrict__ codes, float* __restrict__ scales) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -309,7 +309,7 @@ __global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int rows, i
 
 // dgate of each permuted row = sum over f-tiles of the epilogue partials
 // (fixed order, deterministic), scattered to (source rank, t_local*k+slot).
-__global__ void dgate_reduce_kernel(const float* __restrict__ part, int n_parts,
+static __global__ void dgate_reduce_kernel(const float* __restrict__ part, int n_parts,
                                     const int32_t* __restrict__ row_dst, const int32_t* nrows_pad,
                                     float* const* __restrict__ dst_bufs) {
     const int total = *nrows_pad;
@@ -327,7 +327,7 @@ __global__ void dgate_reduce_kernel(const float* __restrict__ part, int n_parts,
 // pass 2: fixed-order sum over chunks (deterministic). E <= 32 per pass.
 constexpr int kRwChunk = 128;
 template <int EB>
-__global__ void router_wgrad_partial_kernel(const float* __restrict__ dlogits, const uint16_t* __restrict__ x,
+static __global__ void router_wgrad_partial_kernel(const float* __restrict__ dlogits, const uint16_t* __restrict__ x,
                                             int T, int h, int E, float* __restrict__ part) {
     __shared__ float s_dl[kRwChunk * EB];
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -357,7 +357,7 @@ __global__ void router_wgrad_partial_kernel(const float* __restrict__ dlogits, c
     }
 }
 
-__global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int nchunks, int E, int h,
+static __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int nchunks, int E, int h,
                                            float* __restrict__ dwr) {
     const int64_t n = (int64_t)E * h;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -369,7 +369,7 @@ __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int n
 
 // Pack w1 [el][2f][h] ([a | b] rows) into the interleaved layout the fused
 // SwiGLU epilogue expects: per 256-row block, 128 a-rows then 128 b-rows.
-__global__ void pack_w1_kernel(const uint16_t* __restrict__ w1, uint16_t* __restrict__ w1p, int el,
+static __global__ void pack_w1_kernel(const uint16_t* __restrict__ w1, uint16_t* __restrict__ w1p, int el,
                                int f, int h) {
     const int64_t rows = (int64_t)el * 2 * f;
     const int nvec = h / 8;
@@ -386,7 +386,7 @@ __global__ void pack_w1_kernel(const uint16_t* __restrict__ w1, uint16_t* __rest
 
 // Copy this rank's routing (experts/gates for its T_r tokens) into every
 // rank's global routing table at offset rank*T_r*k.
-__global__ void publish_meta_kernel(const int32_t* __restrict__ ex, const float* __restrict__ gt,
+static __global__ void publish_meta_kernel(const int32_t* __restrict__ ex, const float* __restrict__ gt,
                                     int count, int offset, int32_t* const* ex_bufs,
                                     float* const* gt_bufs, int n) {
     for (int p = 0; p < n; ++p)
@@ -402,7 +402,7 @@ __global__ void publish_meta_kernel(const int32_t* __restrict__ ex, const float*
 // is bumped on the device (bump = 1 at the first barrier of a pass), so the
 // whole layer can be captured once in a CUDA graph and replayed. Bounded
 // spin -> *err = 1 on timeout instead of a hang.
-__global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot, int n, int rank,
+static __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot, int n, int rank,
                                     uint32_t* epoch_dev, int bump, unsigned long long timeout_ns,
                                     int* err) {
     __shared__ uint32_t s_epoch;
@@ -434,7 +434,7 @@ __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot, int n
 
 // K1 fast path: router weights staged in shared memory (E*h*2 <= ~200 KB),
 // one warp per token, x streamed with 16-byte loads.
-__global__ void router_logits_smem_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr,
+static __global__ void router_logits_smem_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr,
                                           int T, int h, int E, float* __restrict__ logits) {
     extern __shared__ __align__(16) uint8_t s_raw[];
     uint4* s_w = reinterpret_cast<uint4*>(s_raw);
@@ -477,7 +477,7 @@ __global__ void router_logits_smem_kernel(const uint16_t* __restrict__ x, const 
     }
 }
 
-__global__ void source_rank_kernel(int32_t* src, int T, int tokens_per_rank) {
+static __global__ void source_rank_kernel(int32_t* src, int T, int tokens_per_rank) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
         src[t] = t / tokens_per_rank;
 }
