@@ -35,6 +35,14 @@ CONFIGS = {
                      num_experts=256, top_k=8, tokens_per_rank=4096),
     "small": dict(workload="small-moe-layer-fwd+bwd", hidden=1024, ffn_hidden=2816,
                   num_experts=8, top_k=2, tokens_per_rank=4096),
+    # configs[4]: Mixtral shape, FP8 dispatch/combine, gate after fc2,
+    # Zipf(1.2) routing from the reference's own simulate_routing (golden fixture)
+    "mixtral_fp8_zipf": dict(workload="mixtral-8x7b-moe-layer-fwd+bwd-fp8comm-zipf1.2", hidden=4096,
+                             ffn_hidden=14336, num_experts=8, top_k=2, tokens_per_rank=4096,
+                             comm="fp8", gate="after_fc2_out",
+                             routing_fixture="tests/golden/routing_cfg5_zipf_nodrop_n8.npz"),
+    # configs[3]: sequence-parallel attention QKV / out-proj, hidden 8192, seq 8192, GQA m=8
+    "attn": dict(workload="sp-attention-qkv-ag-gemm+out-proj-gemm-rs", hidden=8192, seq=8192, gqa=8),
 }
 
 
@@ -182,9 +190,20 @@ def run_ours(args, cfg):
     w1 = (torch.randn(el, 2 * f, h, device="cuda", generator=g) / h ** 0.5).bfloat16()
     w2 = (torch.randn(el, h, f, device="cuda", generator=g) / f ** 0.5).bfloat16()
     wr = (torch.randn(E, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7)) / h ** 0.5).bfloat16()
+    injected = "routing_fixture" in cfg
     L = MoELayer(Tr, h, f, E, k, ep_size=n, rank=rank, capacity_factor=0.0,
-                 gate_order="before_fc2_in", route_mode="learned")
+                 gate_order=cfg.get("gate", "before_fc2_in"), comm_format=cfg.get("comm", "bf16"),
+                 route_mode="injected" if injected else "learned")
     L.set_weights(w1, w2, wr)
+    if injected:
+        # routing input data: the reference's simulate_routing output (committed fixture)
+        fx = np.load(os.path.join(ROOT, cfg["routing_fixture"]))
+        ex_all = fx["experts"].astype(np.int32).reshape(-1, k)
+        assert ex_all.shape[0] >= Tr * n, "fixture too small for this many ranks"
+        ex_loc = ex_all[rank * Tr:(rank + 1) * Tr]
+        glog = np.random.default_rng(rank).standard_normal((Tr, k)).astype(np.float32)
+        gates = np.exp(glog) / np.exp(glog).sum(1, keepdims=True)
+        L.set_routing(torch.from_numpy(np.ascontiguousarray(ex_loc)).cuda(), torch.from_numpy(gates).cuda())
     del w1, w2
     if n > 1:
         L.connect()
@@ -355,10 +374,13 @@ def run_ours(args, cfg):
             "metric": "moe_layer_fwd_bwd_tokens_per_s", "value": value, "unit": "tokens/s",
             "n_gpus": n, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (random-init weights, N(0,0.25) tokens; learned router)",
+            "data": ("synthetic (random-init weights, N(0,0.25) tokens; " +
+                     ("injected Zipf routing from the reference's simulate_routing)" if injected else "learned router)")),
             "config": {"workload": cfg["workload"], "hidden": h, "ffn_hidden": f, "num_experts": E,
                        "top_k": k, "tokens_per_rank": Tr, "global_tokens": Tr * n,
-                       "parallelism": f"ep{n}", "l2": "inputs larger than L2 (weights 2.8 GB/layer)"},
+                       "parallelism": f"ep{n}", "comm_format": cfg.get("comm", "bf16"),
+                       "gate_order": cfg.get("gate", "before_fc2_in"),
+                       "l2": "inputs larger than L2 (expert weights >= 2.8 GB/layer)"},
             "roofline": {"bound": "tensor", "kernel": "fc1 grouped GEMM (tcgen05) + fused SwiGLU",
                          "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                          "frac": achieved / peaks["bf16_sus"], "traffic": None,
@@ -391,6 +413,113 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_attn(args, cfg):
+    """configs[3]: fused AG-GEMM (QKV) + GEMM-RS (out-proj) at TP = n, with the
+    NCCL all-gather / reduce-scatter + cuBLAS baseline timed in the same run."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2505_11432_b200 import launch_count, launch_count_reset
+    from paper_2505_11432_b200.attn import AttnProjections
+    n, s_len, h, m = world, cfg["seq"], cfg["hidden"], cfg["gqa"]
+    nq = h * (m + 2) // m // n                 # h (1 + 2/m) / n  (graph.cpp:163-165)
+    dh, sr = h // n, s_len // n
+    g = torch.Generator(device="cuda").manual_seed(3 + rank)
+    wqkv = (torch.randn(nq, h, device="cuda", generator=g) / h ** 0.5).bfloat16()
+    wout = (torch.randn(h, dh, device="cuda", generator=g) / dh ** 0.5).bfloat16()
+    x = (torch.randn(sr, h, device="cuda", generator=g) * 0.5).bfloat16()
+    o = (torch.randn(s_len, dh, device="cuda", generator=g) * 0.5).bfloat16()
+    A = AttnProjections(s_len, h, nq, n, rank)
+    A.set_weights(wqkv, wout)
+    if n > 1:
+        A.connect()
+    A.input_buffer.copy_(x)
+    qkv = torch.empty(s_len, nq, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(sr, h, dtype=torch.bfloat16, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        A.ag_gemm(None, qkv)
+        A.gemm_rs(o, y)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if n > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        sync_all()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
+        sync_all()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        if n > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    launch_count_reset()
+    step()
+    per_step = launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms = timed(step)
+    clk = clocks.stop()
+    ms_ag = timed(lambda: A.ag_gemm(None, qkv))
+    # NCCL + cuBLAS baseline for the same math
+    xg = torch.empty(s_len, h, dtype=torch.bfloat16, device="cuda")
+    part = torch.empty(s_len, h, dtype=torch.bfloat16, device="cuda")
+
+    def nccl_step():
+        if n > 1:
+            dist.all_gather_into_tensor(xg, x)
+        else:
+            xg.copy_(x)
+        torch.matmul(xg, wqkv.T, out=qkv)
+        torch.matmul(o, wout.T, out=part)
+        if n > 1:
+            dist.reduce_scatter_tensor(y, part)
+        else:
+            y.copy_(part)
+    ms_nccl = timed(nccl_step)
+    if rank == 0:
+        peaks = load_peaks()
+        flops = 2.0 * s_len * h * nq + 2.0 * s_len * dh * h
+        link_bytes = 2.0 * (n - 1) / n * s_len * h * 2 if n > 1 else 0.0
+        t_tensor = flops / (peaks["bf16"] * 1e12)
+        t_link = link_bytes / 770e9
+        line = {
+            "metric": "sp_attention_projection_pair_tokens_per_s", "value": s_len / (ms / 1000.0),
+            "unit": "tokens/s", "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "hidden": h, "seq": s_len, "gqa_ratio": m,
+                       "qkv_cols_per_rank": nq, "parallelism": f"tp{n}-sp{n}"},
+            "roofline": {"bound": "nvlink" if t_link > t_tensor else "tensor",
+                         "target_ms": 1000 * max(t_tensor, t_link), "achieved_ms": ms,
+                         "frac": 1000 * max(t_tensor, t_link) / ms,
+                         "peak": "bf16 %.1f TF (measured burst), NVLink 770 GB/s/dir (measured ref.)" % peaks["bf16"]},
+            "ag_gemm_ms": ms_ag, "gemm_rs_ms": ms - ms_ag,
+            "nccl_cublas_baseline_ms": ms_nccl, "speedup_vs_nccl_baseline": ms_nccl / ms,
+            "clocks": clk, "gpu_launches": per_step * args.steps, "launch_mode": "eager",
+            "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    if n > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -406,6 +535,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.config == "attn":
+        run_attn(args, cfg)
     else:
         run_ours(args, cfg)
 

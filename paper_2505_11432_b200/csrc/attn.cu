@@ -192,6 +192,7 @@ moe_status moe_attn_ag_gemm(moe_attn* A, const uint16_t* d_x_shard, uint16_t* d_
     a.K = (int)A->h;
     a.out = d_qkv;
     a.ldo = A->nq;
+    a.m_chunk = 4;  // first wave waits for 4 row blocks, not the whole gather
     a.pad_row_tok = A->ident;
     a.nrows_pad = A->rows_pad;
     a.src_bufs = reinterpret_cast<const uint16_t* const*>(A->tab);

@@ -58,6 +58,9 @@ struct GemmArgs {
     void* const* rank_base;     // SCATTER: per destination rank base pointer
     int gate_rows;              // 1: multiply rows by row_gate in STORE/SCATTER epilogue
     int b_box_rows;             // K-major B: rows per TMA box (0 = whole tile half)
+    int m_chunk;                // M-grouped raster: m-tiles per chunk (0 = whole group, m fastest).
+                                // Fused-dispatch GEMMs use small chunks so the first wave only
+                                // needs the first rows to arrive.
     int interleave_rows;        // K-grouped STORE: map packed a/b-interleaved rows back to
                                 // the reference [a | b] row order (dW1)
     // fused dispatch (AG + local scatter into the A operand, DISPATCH = true)
@@ -85,13 +88,14 @@ struct GemmCfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN_CTA * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+    static constexpr int EPI_STAGE_BYTES = 8 * 2048;  // per epilogue warp: 32 x 32 bf16 transpose tile
+    static constexpr int STAGES = (206 * 1024) / STAGE_BYTES > 8 ? 8 : (206 * 1024) / STAGE_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int MAX_GROUPS = 256;
     static constexpr int EPI_WARPS = 8;
     static constexpr int COMM_WARPS = 2;   // only launched for the fused-dispatch variant
     static constexpr int THREADS = 64 + EPI_WARPS * 32;
-    static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES +
+    static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_STAGE_BYTES +
                                       (2 * STAGES + 4) * 8 + 16;
 };
 
@@ -114,8 +118,13 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
     int li = t - prefix[lo];
     if (!K_GROUPED) {
         const int mt = a.group_rows[lo] / TILE_M;
-        ti.n = li / mt;
-        ti.m = li - ti.n * mt;
+        const int mc = (a.m_chunk > 0 && a.m_chunk < mt) ? a.m_chunk : mt;
+        const int full = mc * n_tiles;
+        const int c = li / full;
+        const int r = li - c * full;
+        const int cm = min(mc, mt - c * mc);
+        ti.n = r / cm;
+        ti.m = c * mc + (r - ti.n * cm);
         ti.kblocks = (a.K + 63) / 64;
         ti.row0 = row_off[lo] + ti.m * TILE_M;
     } else {
@@ -185,13 +194,60 @@ __device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr) {
                  : "memory");
 }
 
+// ---- coalesced row I/O through a per-warp 2 KB shared-memory tile ----------
+// The accumulator gives each lane one row; global rows are far apart. These
+// helpers transpose a 32-row x 32-column bf16 chunk so that every global
+// access instruction covers 8 rows x 64 contiguous bytes (4 lanes per row)
+// instead of 32 rows x 16 bytes. XOR swizzle on (row >> 1) & 3 keeps both
+// the row-wise and the column-wise shared-memory phases conflict-free.
+__device__ __forceinline__ int xs_idx(int row, int u) { return row * 4 + (u ^ ((row >> 1) & 3)); }
+
+__device__ __forceinline__ void store_rows32(uint4* wst, const uint32_t (&pk)[16], void* row_ptr, int lane) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wst[xs_idx(lane, u)] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+    __syncwarp();
+    const unsigned long long my = reinterpret_cast<unsigned long long>(row_ptr);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int R = (lane >> 2) + 8 * i, c = lane & 3;
+        const unsigned long long p = __shfl_sync(0xffffffffu, my, R);
+        const uint4 v = wst[xs_idx(R, c)];
+        if (p) reinterpret_cast<uint4*>(p)[c] = v;
+    }
+    __syncwarp();
+}
+
+// Issue the coalesced global loads of a 32 x 32 bf16 chunk (4 x 16 B per lane).
+__device__ __forceinline__ void load_rows32_issue(uint4 (&v)[4], const void* row_ptr, int lane) {
+    const unsigned long long my = reinterpret_cast<unsigned long long>(row_ptr);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int R = (lane >> 2) + 8 * i, c = lane & 3;
+        const unsigned long long p = __shfl_sync(0xffffffffu, my, R);
+        v[i] = reinterpret_cast<const uint4*>(p)[c];
+    }
+}
+// ... and transpose them so this lane ends up with its own row's 16 words.
+__device__ __forceinline__ void load_rows32_finish(uint4* wst, const uint4 (&v)[4], uint32_t (&pk)[16], int lane) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wst[xs_idx((lane >> 2) + 8 * i, lane & 3)] = v[i];
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint4 x = wst[xs_idx(lane, u)];
+        pk[4 * u] = x.x; pk[4 * u + 1] = x.y; pk[4 * u + 2] = x.z; pk[4 * u + 3] = x.w;
+    }
+    __syncwarp();
+}
+
 // ---- epilogue ---------------------------------------------------------------
 // One warp handles 32 rows (its TMEM lane quarter) x `ncols` columns starting
 // at column c_lo of the BN-wide accumulator.
 template <int BN, int EPI, bool K_GROUPED>
 __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileInfo& ti,
                                               int64_t orow, uint32_t tbase, int c_lo,
-                                              int half, int n_tiles) {
+                                              int half, int n_tiles, uint4* wst) {
+    const int lane = threadIdx.x & 31;
     const int n0 = ti.n * BN;
     constexpr int HALF = BN / 2;
     if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_STORE_F32 || EPI == EPI_SCATTER) {
@@ -216,7 +272,16 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             uint32_t r[32];
             tmem_ld32(tbase + c0, r);
             tmem_ld_wait();
-            if (!valid || n0 + c0 >= args.N) continue;
+            if (n0 + c0 >= args.N) continue;   // warp-uniform
+            if (EPI != EPI_STORE_F32) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]) * gscale, __uint_as_float(r[2 * q + 1]) * gscale);
+                store_rows32(wst, pk, valid ? (void*)(obf + c0) : nullptr, lane);
+                continue;
+            }
+            if (!valid) continue;
             if (EPI == EPI_STORE_F32) {
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
@@ -289,22 +354,19 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             tmem_ld32(tbase + c0, ra);
             tmem_ld32(tbase + HALF + c0, rb);
             tmem_ld_wait();
+            uint32_t pa[16], pb[16], ph[16];
 #pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-                uint32_t pa[4], pb[4], ph[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    pa[q] = pack_bf16x2(__uint_as_float(ra[i + 2 * q]), __uint_as_float(ra[i + 2 * q + 1]));
-                    pb[q] = pack_bf16x2(__uint_as_float(rb[i + 2 * q]), __uint_as_float(rb[i + 2 * q + 1]));
-                    // SwiGLU on the bf16-rounded fc1_out so backward remat is exact
-                    const float2 a2 = unpack_bf16x2(pa[q]);
-                    const float2 b2 = unpack_bf16x2(pb[q]);
-                    ph[q] = pack_bf16x2(a2.x * silu_f(b2.x) * g, a2.y * silu_f(b2.y) * g);
-                }
-                *reinterpret_cast<uint4*>(o1 + c0 + i) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-                *reinterpret_cast<uint4*>(o1 + HALF + c0 + i) = make_uint4(pb[0], pb[1], pb[2], pb[3]);
-                *reinterpret_cast<uint4*>(o2 + c0 + i) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+            for (int q = 0; q < 16; ++q) {
+                pa[q] = pack_bf16x2(__uint_as_float(ra[2 * q]), __uint_as_float(ra[2 * q + 1]));
+                pb[q] = pack_bf16x2(__uint_as_float(rb[2 * q]), __uint_as_float(rb[2 * q + 1]));
+                // SwiGLU on the bf16-rounded fc1_out so backward remat is exact
+                const float2 a2 = unpack_bf16x2(pa[q]);
+                const float2 b2 = unpack_bf16x2(pb[q]);
+                ph[q] = pack_bf16x2(a2.x * silu_f(b2.x) * g, a2.y * silu_f(b2.y) * g);
             }
+            store_rows32(wst, pa, o1 + c0, lane);
+            store_rows32(wst, pb, o1 + HALF + c0, lane);
+            store_rows32(wst, ph, o2 + c0, lane);
         }
     } else if constexpr (EPI == EPI_SWIGLU_BWD) {
         // D = d fc2_in for f-columns [n0 + c_lo, +BN/2). fc1_out / dfc1 use the
@@ -314,40 +376,24 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         uint16_t* d1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo;
         uint16_t* rf = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2;
         float dg = 0.0f;
-        // software-pipelined fc1_out loads: chunk c+1 in flight while c computes
-        uint4 av[4], bv[4], an[4], bn[4];
-        {
-            const int j = n0 + c_lo;
-            const int ia = (j >> 7) * 256 + (j & 127);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                av[q] = *reinterpret_cast<const uint4*>(f1 + ia + q * 8);
-                bv[q] = *reinterpret_cast<const uint4*>(f1 + ia + 128 + q * 8);
-            }
-        }
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             const int j = n0 + c0;           // f column
             const int ia = (j >> 7) * 256 + (j & 127);
-            if (c0 + 32 < c_lo + HALF) {
-                const int jn = j + 32;
-                const int ian = (jn >> 7) * 256 + (jn & 127);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    an[q] = *reinterpret_cast<const uint4*>(f1 + ian + q * 8);
-                    bn[q] = *reinterpret_cast<const uint4*>(f1 + ian + 128 + q * 8);
-                }
-            }
+            uint4 va[4], vb[4];
+            load_rows32_issue(va, f1 + ia, lane);        // coalesced fc1_out loads in flight
+            load_rows32_issue(vb, f1 + ia + 128, lane);  // while the accumulator is read
             uint32_t r[32];
             tmem_ld32(tbase + c0, r);
             tmem_ld_wait();
+            uint32_t aw[16], bw[16];
+            load_rows32_finish(wst, va, aw, lane);
+            load_rows32_finish(wst, vb, bw, lane);
             uint32_t da[16], db[16], hf[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                const uint32_t aw = (&av[q >> 2].x)[q & 3];
-                const uint32_t bw = (&bv[q >> 2].x)[q & 3];
-                const float2 a2 = unpack_bf16x2(aw);
-                const float2 b2 = unpack_bf16x2(bw);
+                const float2 a2 = unpack_bf16x2(aw[q]);
+                const float2 b2 = unpack_bf16x2(bw[q]);
                 const float d0 = __uint_as_float(r[2 * q]), d1v = __uint_as_float(r[2 * q + 1]);
                 const float s0 = 1.0f / (1.0f + __expf(-b2.x)), s1 = 1.0f / (1.0f + __expf(-b2.y));
                 const float si0 = b2.x * s0, si1 = b2.y * s1;
@@ -357,17 +403,9 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                                     d1v * g * a2.y * s1 * (1.0f + b2.y * (1.0f - s1)));
                 hf[q] = pack_bf16x2(a2.x * si0 * g, a2.y * si1 * g);
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                *reinterpret_cast<uint4*>(d1 + ia + q * 8) = make_uint4(da[4 * q], da[4 * q + 1], da[4 * q + 2], da[4 * q + 3]);
-                *reinterpret_cast<uint4*>(d1 + ia + 128 + q * 8) = make_uint4(db[4 * q], db[4 * q + 1], db[4 * q + 2], db[4 * q + 3]);
-                *reinterpret_cast<uint4*>(rf + j + q * 8) = make_uint4(hf[4 * q], hf[4 * q + 1], hf[4 * q + 2], hf[4 * q + 3]);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                av[q] = an[q];
-                bv[q] = bn[q];
-            }
+            store_rows32(wst, da, d1 + ia, lane);
+            store_rows32(wst, db, d1 + ia + 128, lane);
+            store_rows32(wst, hf, rf + j, lane);
         }
         if (args.row_part) args.row_part[orow * (2 * n_tiles) + ti.n * 2 + half] = dg;
     }
@@ -453,7 +491,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+    uint4* epi_stage = reinterpret_cast<uint4*>(smem + STAGES * Cfg::STAGE_BYTES);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_STAGE_BYTES);
     uint64_t* empty_bar = full_bar + STAGES;
     uint64_t* tfull_bar = empty_bar + STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -653,7 +692,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-            epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, half * (BN / 2), half, n_tiles);
+            epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, half * (BN / 2), half, n_tiles,
+                                              epi_stage + ew * 128);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {

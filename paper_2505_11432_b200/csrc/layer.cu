@@ -189,6 +189,7 @@ moe_status build_plans(moe_layer* L) {
 
 // Fused dispatch (AG + local scatter) of one of the two pulled operands.
 void set_dispatch(moe_layer* L, GemmArgs& a, bool backward, uint16_t* dst) {
+    if (L->fused_dispatch) a.m_chunk = 8;  // first wave needs only the first 8 row blocks
     a.pad_row_tok = L->pad_tok;
     a.nrows_pad = L->gpad_off + L->el;
     a.a_dst = dst;
