@@ -32,12 +32,17 @@ compat: $(LIB)
 	@if [ -d "$(REF)/core/include" ]; then \
 	  g++ -std=c++20 -O2 -fPIC -shared -Ioracle/shim -I$(JSON_INC) -I$(REF)/core/include \
 	    -I/usr/local/cuda/include -o $(COMPAT) $(PKG)/compat/moeplan_compat.cpp \
+	    $(PKG)/compat/moeplan_numerics_compat.cpp \
 	    -L$(PKG) -lmoe_b200 -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN' && \
 	  mkdir -p oracle/_ref && \
 	  g++ -std=c++20 -O2 -Itests/doctest_shim -Ioracle/shim -I$(JSON_INC) -I$(REF)/core/include \
 	    -I$(REF)/tests -o oracle/_ref/ref_test_routing_on_gpu $(REF)/tests/test_routing.cpp \
 	    -L$(PKG) -lmoeplan_compat -lmoe_b200 -L/usr/local/cuda/lib64 -lcudart \
-	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' && echo "built compat adapter + reference test binary"; \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' && \
+	  g++ -std=c++20 -O2 -Itests/doctest_shim -Ioracle/shim -I$(JSON_INC) -I$(REF)/core/include \
+	    -I$(REF)/tests -o oracle/_ref/ref_test_numerics_on_gpu $(REF)/tests/test_numerics.cpp \
+	    -L$(PKG) -lmoeplan_compat -lmoe_b200 -L/usr/local/cuda/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' && echo "built compat adapter + reference test binaries"; \
 	else echo "reference headers absent: using prebuilt $(COMPAT)"; fi
 
 clean:

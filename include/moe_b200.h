@@ -136,6 +136,30 @@ moe_status moe_quantize_e4m3_rows(const uint16_t* d_x, int64_t rows, int64_t col
 moe_status moe_quantize_e4m3_rows_f32(const float* d_x, int64_t rows, int64_t cols,
                                       uint8_t* d_codes, float* d_scales, moe_stream_t stream);
 
+/* Reference numerics, bit-exact (binary64 on the device, same operation
+ * order). fmt: 0 fp32, 1 bf16, 2 fp8_e4m3 (config.hpp:41); gran: 0
+ * per_tensor, 1 per_token, 2 per_channel, 3 grouped (numerics.hpp:41);
+ * kind: 0 ring_bf16, 1 a2a_fp32 (numerics.hpp:64). */
+/* Replaces numerics::round_to (numerics.hpp:31). */
+moe_status moe_round_to(int32_t fmt, const double* d_x, int64_t n, double* d_out, moe_stream_t stream);
+/* Replaces numerics::quantize (numerics.hpp:61-62): codes [rows*cols],
+ * scales [moe_quantize_num_blocks(...)], workspace moe_quantize_workspace_size. */
+int64_t moe_quantize_num_blocks(int64_t rows, int64_t cols, int32_t gran, int64_t group_size);
+size_t moe_quantize_workspace_size(int64_t rows, int64_t cols, int32_t gran, int64_t group_size);
+moe_status moe_quantize(const double* d_x, int64_t rows, int64_t cols, int32_t gran, int64_t group_size,
+                        int32_t fmt, double* d_codes, double* d_scales, void* d_workspace,
+                        moe_stream_t stream);
+/* Replaces Quantized::dequantize (numerics.hpp:57). */
+moe_status moe_dequantize(const double* d_codes, const double* d_scales, int64_t rows, int64_t cols,
+                          int32_t gran, int64_t group_size, double* d_out, moe_stream_t stream);
+/* Replaces numerics::emulate_reduce (numerics.hpp:77-78); vectors [ranks, dim]. */
+moe_status moe_emulate_reduce(const double* d_vectors, int64_t ranks, int64_t dim, int32_t kind,
+                              double* d_out, moe_stream_t stream);
+/* SwiGLU a*silu(b) over [a | b] rows in binary64, optional per-row weight
+ * (numerics.cpp:262-268). */
+moe_status moe_swiglu_rows_f64(const double* d_x, int64_t rows, int64_t cols, const double* d_row_weight,
+                               double* d_out, moe_stream_t stream);
+
 /* ===================================================================== */
 /* MoE layer (router -> dispatch -> fc1/SwiGLU -> fc2 -> combine)          */
 /* ===================================================================== */

@@ -33,7 +33,8 @@ def test_compat_adapter_exports():
         pytest.skip("compat adapter not built")
     out = os.popen(f"nm -DC {path}").read()
     for sym in ("moeplan::routing::build_scatter_map", "moeplan::routing::sort_tokens_for_tiles",
-                "moeplan::routing::balance_metrics", "moeplan::routing::simulate_routing"):
+                "moeplan::routing::balance_metrics", "moeplan::routing::simulate_routing",
+                "moeplan::numerics::quantize", "moeplan::numerics::emulate_reduce"):
         assert sym in out, sym
 
 
