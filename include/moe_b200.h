@@ -275,6 +275,18 @@ moe_status moe_layer_ipc_export(moe_layer* L, void* h_blob);
  * order) and map peer buffers. Call once after every rank exported. */
 moe_status moe_layer_ipc_import(moe_layer* L, const void* h_blobs);
 
+/* fp32 MoE layer forward on one GPU (BASELINE configs[0]): router (fp32;
+ * skipped when d_experts_in/d_gates_in are given) -> capacity drop (cf <= 0:
+ * none) -> permutation -> dispatch -> fc1 -> SwiGLU (-> gate) -> fc2 ->
+ * gather -> combine, all in fp32 (FFMA expert GEMMs). Weights in the
+ * reference layout w1 [E][2f][h] ([a|b] rows), w2 [E][h][f], wr [E][h]. */
+moe_status moe_ffn_forward_f32(const float* d_x, const float* d_w1, const float* d_w2,
+                               const float* d_wr, int64_t T, int64_t h, int64_t f, int64_t E,
+                               int64_t k, double capacity_factor, int32_t gate_order,
+                               const int32_t* d_experts_in, const float* d_gates_in, float* d_y,
+                               int32_t* d_experts, float* d_gates, float* d_logits,
+                               uint8_t* d_dropped, moe_stream_t stream);
+
 /* ===================================================================== */
 /* Sequence-parallel attention projections (TP weights, SP activations)   */
 /* reference nodes ag_attn_in + qkv_proj, out_proj + rs_attn_out,          */

@@ -44,3 +44,25 @@ def quantize_e4m3_rows(x: torch.Tensor, stream=None):
     else:
         raise DomainError("quantize takes fp32 or bf16")
     return codes, scales
+
+
+def ffn_forward_f32(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor, wr: torch.Tensor | None, k: int,
+                    capacity_factor: float = 0.0, gate_order: str = "before_fc2_in", experts=None, gates=None,
+                    stream=None):
+    """fp32 MoE layer forward (configs[0]); returns y, experts, gates, logits, dropped."""
+    import ctypes as C
+    require_cuda(x, w1, w2)
+    T, h = x.shape
+    E, f2, _ = w1.shape
+    dev = x.device
+    y = torch.empty(T, h, dtype=torch.float32, device=dev)
+    ex = torch.empty(T, k, dtype=torch.int32, device=dev)
+    g = torch.empty(T, k, dtype=torch.float32, device=dev)
+    lg = torch.empty(T, E, dtype=torch.float32, device=dev)
+    dr = torch.empty(T, dtype=torch.uint8, device=dev)
+    check(lib().moe_ffn_forward_f32(ptr(x.contiguous()), ptr(w1.contiguous()), ptr(w2.contiguous()),
+                                    ptr(None if wr is None else wr.contiguous()), i64(T), i64(h), i64(f2 // 2),
+                                    i64(E), i64(k), C.c_double(capacity_factor),
+                                    int(gate_order.startswith("after")), ptr(experts), ptr(gates), ptr(y),
+                                    ptr(ex), ptr(g), ptr(lg), ptr(dr), stream_ptr(stream)))
+    return y, ex, g, lg, dr
