@@ -189,7 +189,9 @@ moe_status build_plans(moe_layer* L) {
 
 // Fused dispatch (AG + local scatter) of one of the two pulled operands.
 void set_dispatch(moe_layer* L, GemmArgs& a, bool backward, uint16_t* dst) {
-    if (L->fused_dispatch) a.m_chunk = 8;  // first wave needs only the first 8 row blocks
+    // with peers to pull from, the first wave should need only the first 8
+    // row blocks; on one GPU the whole-group raster reads each weight once
+    if (L->fused_dispatch && L->n > 1 && !L->comm_local) a.m_chunk = 8;
     a.pad_row_tok = L->pad_tok;
     a.nrows_pad = L->gpad_off + L->el;
     a.a_dst = dst;
