@@ -167,6 +167,11 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def routing_probe_rows(L, rank, el):
+    cnt = L.routing()["per_expert_counts"].cpu().tolist()[rank * el:(rank + 1) * el]
+    return int(sum((c + 255) // 256 * 256 for c in cnt))
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -300,6 +305,23 @@ def run_ours(args, cfg):
         L.backward(dy, dx, dw1, dw2, dwr)   # back to back: no idle gap between phases
         for kk, v in L.phase_times().items():
             phases[kk] = phases.get(kk, 0.0) + v / reps
+    # memory-bound operators with the unfused dispatch (the reference's separate
+    # scatter node) for their achieved HBM bandwidth
+    membw = None
+    if cfg.get("comm", "bf16") == "bf16" and cfg.get("gate", "before_fc2_in") == "before_fc2_in":
+        L.set_fused_dispatch(False)
+        L.forward(None, y)
+        L.backward(dy, dx, dw1, dw2, dwr)
+        pu = L.phase_times()
+        L.set_fused_dispatch(True)
+        rows_pad = routing_probe_rows(L, rank, el)
+        hbm = load_peaks()["hbm"]
+        rb = Tr * h * 2 + E * h * 2              # router: x + W_r
+        sb = 2 * rows_pad * h * 2                # scatter: read rows + write permuted rows
+        cb = (k + 1) * Tr * h * 2                # combine: k staged rows in + y out
+        membw = {kk: {"ms": pu[ph], "GBps": b / (pu[ph] * 1e6), "frac_hbm": b / (pu[ph] * 1e6) / hbm}
+                 for kk, ph, b in (("router", "route", rb), ("scatter", "dispatch", sb), ("combine", "combine", cb))
+                 if ph in pu and pu[ph] > 0}
     L.enable_timing(False)
     sync_all()
 
@@ -389,6 +411,7 @@ def run_ours(args, cfg):
                          "step_frac": total_flops / (ms / 1000.0) / 1e12 / peaks["bf16_sus"]},
             "phases_ms": {kk: round(v, 4) for kk, v in phases.items()},
             "routing_rank0": routing_info,
+            "memory_bound_ops": membw,
             "exposed_comm": exposed,
             "clocks": clk,
             "gpu_launches": int(launches),

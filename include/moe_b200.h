@@ -254,6 +254,11 @@ moe_status moe_layer_phase_times(moe_layer* L, float* h_ms, int max_phases, int*
  * not meaningful in that mode; 0 restores normal operation. */
 moe_status moe_layer_set_comm_mode(moe_layer* L, int compute_only);
 
+/* 1 (default): dispatch (AG + local scatter) fused into the fc1 / fc2-dgrad
+ * GEMMs; 0: a separate memory-bound scatter kernel (the reference's unfused
+ * operator structure, graph.cpp:276-286; used to measure it). */
+moe_status moe_layer_set_fused_dispatch(moe_layer* L, int fused);
+
 /* Non-zero if a cross-GPU flag wait of this layer timed out (synchronous). */
 int moe_layer_error_flag(moe_layer* L);
 

@@ -43,13 +43,11 @@ class AttnProjections:
         check(lib().moe_attn_set_weights(self._h, ptr(self._keep[0]), ptr(self._keep[1]), stream_ptr(stream)))
 
     def connect(self, group=None):
-        import torch.distributed as dist
+        from .dist import exchange_blobs
         sz = int(lib().moe_attn_ipc_handle_size())
         blob = (C.c_uint8 * sz)()
         check(lib().moe_attn_ipc_export(self._h, blob))
-        allb = [None] * self.n
-        dist.all_gather_object(allb, bytes(blob), group=group)
-        joined = b"".join(allb)
+        joined = exchange_blobs(bytes(blob), self.n, group)
         check(lib().moe_attn_ipc_import(self._h, (C.c_uint8 * len(joined)).from_buffer_copy(joined)))
 
     def ag_gemm(self, x_shard=None, out=None, stream=None):

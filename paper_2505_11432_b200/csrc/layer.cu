@@ -772,6 +772,14 @@ moe_status moe_layer_ipc_import(moe_layer* L, const void* h_blobs) {
     return MOE_OK;
 }
 
+moe_status moe_layer_set_fused_dispatch(moe_layer* L, int fused) {
+    MOE_CHECK_ARG(L, "null argument");
+    MOE_CHECK_ARG(fused || (!L->fp8 && !L->gate_after),
+                  "the unfused dispatch path supports bf16 comm with gate before fc2 only");
+    L->fused_dispatch = fused != 0;
+    return MOE_OK;
+}
+
 moe_status moe_layer_set_comm_mode(moe_layer* L, int compute_only) {
     MOE_CHECK_ARG(L, "null argument");
     L->comm_local = compute_only != 0;

@@ -447,6 +447,7 @@ static __global__ void router_logits_smem_kernel(const uint16_t* __restrict__ x,
         const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)t * h);
         for (int e0 = 0; e0 < E; e0 += 8) {
             float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
             for (int v = lane; v < nvec; v += 32) {
                 const uint4 xv = __ldg(xr + v);
                 const float2 x0 = unpack_bf16x2(xv.x), x1 = unpack_bf16x2(xv.y),

@@ -151,6 +151,9 @@ class MoELayer:
         check(lib().moe_layer_phase_times(self._h, ms, 32, C.byref(cnt), names))
         return {names[i].decode(): ms[i] for i in range(cnt.value)}
 
+    def set_fused_dispatch(self, on: bool):
+        check(lib().moe_layer_set_fused_dispatch(self._h, int(bool(on))))
+
     def set_compute_only(self, on: bool):
         """Exposed-comm measurement mode (see moe_layer_set_comm_mode)."""
         check(lib().moe_layer_set_comm_mode(self._h, int(bool(on))))
@@ -161,13 +164,10 @@ class MoELayer:
     # ------------------------------------------------------------------
     def connect(self, group=None):
         """Exchange IPC handles with every rank (collective over torch.distributed)."""
-        import torch.distributed as dist
+        from .dist import exchange_blobs
         sz = int(lib().moe_layer_ipc_handle_size())
         blob = (C.c_uint8 * sz)()
         check(lib().moe_layer_ipc_export(self._h, blob))
-        mine = bytes(blob)
-        allb = [None] * self.n
-        dist.all_gather_object(allb, mine, group=group)
-        joined = b"".join(allb)
+        joined = exchange_blobs(bytes(blob), self.n, group)
         buf = (C.c_uint8 * len(joined)).from_buffer_copy(joined)
         check(lib().moe_layer_ipc_import(self._h, buf))
