@@ -430,6 +430,10 @@ def run_ours(args, cfg):
                               f"router+FFN fwd+bwd incl. weight grads ({cores} OpenMP threads)"}
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        if args.trace:
+            from paper_2505_11432_b200.trace import write_trace
+            write_trace(args.trace, phases, Tr * k, h, f,
+                        exposed["exposed_ms"] / 1000.0 if exposed else None)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -553,6 +557,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
+    ap.add_argument("--trace", default=None, help="write the measured per-phase timeline (reference trace schema)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
