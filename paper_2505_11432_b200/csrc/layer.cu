@@ -174,7 +174,7 @@ moe_status build_plans(moe_layer* L) {
         p->cg = L->cg;
     // router logits[T_r, E] = x . wr^T on the tensor cores when W_r does not
     // fit in shared memory (DeepSeek shape: E = 256, h = 7168)
-    L->gemm_router = (size_t)L->E * h * 2 > 200 * 1024 || L->E > 64;
+    L->gemm_router = (size_t)L->E * h * 4 > 200 * 1024 || L->E > 64;
     if (L->gemm_router) {
         L->p_router = GemmPlan{};
         L->p_router.epi = EPI_STORE_F32;
@@ -436,7 +436,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         MOE_CUDA_TRY(cudaMemcpyAsync(x_sym, d_x, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
     // K1 router (learned mode)
     if (L->cfg.route_mode == 0) {
-        const size_t wbytes = (size_t)L->E * h * 2;
+        const size_t wbytes = (size_t)L->E * h * 4;  // fp32 in shared memory
         if (L->gemm_router) {
             GemmArgs a{};
             a.G = 1;
@@ -454,7 +454,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
                 L->router_attr = true;
             }
-            router_logits_smem_kernel<<<kNumSMs, 512, wbytes, s>>>(x_sym, L->wr, (int)Tr, (int)h,
+            router_logits_smem_kernel<<<kNumSMs, 256, wbytes, s>>>(x_sym, L->wr, (int)Tr, (int)h,
                                                                    (int)L->E, L->logits);
             count_launch();
             MOE_TRY(launch_topk_from_logits(L->logits, Tr, L->E, k, L->ex_loc, L->gt_loc, s));

@@ -126,6 +126,7 @@ static __global__ void combine_reduce_kernel(const void* __restrict__ stage_v, c
                 }
             }
         }
+#pragma unroll 2
         for (int v = lane; v < nv16; v += 32) {
             float acc[16];
 #pragma unroll
@@ -432,48 +433,80 @@ static __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot
     __syncthreads();
 }
 
-// K1 fast path: router weights staged in shared memory (E*h*2 <= ~200 KB),
-// one warp per token, x streamed with 16-byte loads.
-static __global__ void router_logits_smem_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr,
-                                          int T, int h, int E, float* __restrict__ logits) {
-    extern __shared__ __align__(16) uint8_t s_raw[];
-    uint4* s_w = reinterpret_cast<uint4*>(s_raw);
-    const int nvec = h / 8;
-    for (int i = threadIdx.x; i < E * nvec; i += blockDim.x) s_w[i] = reinterpret_cast<const uint4*>(wr)[i];
+// K1 fast path: router weights staged in shared memory as fp32 (E*h*4 bytes),
+// one warp per FOUR tokens so every shared-memory weight load feeds four
+// FMAs (the kernel is bound by x's HBM stream, not by shared memory),
+// x streamed with 16-byte loads. E is processed in groups of 8.
+static __global__ void __launch_bounds__(256, 1) router_logits_smem_kernel(
+    const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr, int T, int h, int E,
+    float* __restrict__ logits) {
+    extern __shared__ __align__(16) float s_wf[];  // [E][h] fp32
+    for (int i = threadIdx.x; i < E * h / 8; i += blockDim.x) {
+        const uint4 v = reinterpret_cast<const uint4*>(wr)[i];
+        const float2 a = unpack_bf16x2(v.x), b = unpack_bf16x2(v.y), c = unpack_bf16x2(v.z), d = unpack_bf16x2(v.w);
+        reinterpret_cast<float4*>(s_wf)[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+        reinterpret_cast<float4*>(s_wf)[2 * i + 1] = make_float4(c.x, c.y, d.x, d.y);
+    }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
-    for (int t = blockIdx.x * wpb + warp; t < T; t += gridDim.x * wpb) {
-        const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)t * h);
+    const int nvec = h / 8;
+    for (int t0 = (blockIdx.x * wpb + warp) * 4; t0 < T; t0 += gridDim.x * wpb * 4) {
+        const int nt = min(4, T - t0);
         for (int e0 = 0; e0 < E; e0 += 8) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
+            float acc[4][8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[i][q] = 0.0f;
+            // software-pipelined x stream: next 16-byte vectors in flight while
+            // the current ones are multiplied
+            uint4 xn[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                xn[i] = (i < nt && lane < nvec) ? __ldg(reinterpret_cast<const uint4*>(x + (int64_t)(t0 + i) * h) + lane)
+                                               : make_uint4(0, 0, 0, 0);
             for (int v = lane; v < nvec; v += 32) {
-                const uint4 xv = __ldg(xr + v);
-                const float2 x0 = unpack_bf16x2(xv.x), x1 = unpack_bf16x2(xv.y),
-                             x2 = unpack_bf16x2(xv.z), x3 = unpack_bf16x2(xv.w);
+                float xf[4][8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint4 xv = xn[i];
+                    const float2 a = unpack_bf16x2(xv.x), b = unpack_bf16x2(xv.y),
+                                 c = unpack_bf16x2(xv.z), d = unpack_bf16x2(xv.w);
+                    xf[i][0] = a.x; xf[i][1] = a.y; xf[i][2] = b.x; xf[i][3] = b.y;
+                    xf[i][4] = c.x; xf[i][5] = c.y; xf[i][6] = d.x; xf[i][7] = d.y;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    xn[i] = (i < nt && v + 32 < nvec)
+                                ? __ldg(reinterpret_cast<const uint4*>(x + (int64_t)(t0 + i) * h) + v + 32)
+                                : make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     if (e0 + q < E) {
-                        const uint4 wv = s_w[(e0 + q) * nvec + v];
-                        const float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y),
-                                     w2 = unpack_bf16x2(wv.z), w3 = unpack_bf16x2(wv.w);
-                        float a = acc[q];
-                        a = fmaf(x0.x, w0.x, a); a = fmaf(x0.y, w0.y, a);
-                        a = fmaf(x1.x, w1.x, a); a = fmaf(x1.y, w1.y, a);
-                        a = fmaf(x2.x, w2.x, a); a = fmaf(x2.y, w2.y, a);
-                        a = fmaf(x3.x, w3.x, a); a = fmaf(x3.y, w3.y, a);
-                        acc[q] = a;
+                        const float4 w0 = reinterpret_cast<const float4*>(s_wf + (int64_t)(e0 + q) * h)[2 * v];
+                        const float4 w1 = reinterpret_cast<const float4*>(s_wf + (int64_t)(e0 + q) * h)[2 * v + 1];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            float s = acc[i][q];
+                            s = fmaf(xf[i][0], w0.x, s); s = fmaf(xf[i][1], w0.y, s);
+                            s = fmaf(xf[i][2], w0.z, s); s = fmaf(xf[i][3], w0.w, s);
+                            s = fmaf(xf[i][4], w1.x, s); s = fmaf(xf[i][5], w1.y, s);
+                            s = fmaf(xf[i][6], w1.z, s); s = fmaf(xf[i][7], w1.w, s);
+                            acc[i][q] = s;
+                        }
                     }
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                float a = acc[q];
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-                if (lane == 0 && e0 + q < E) logits[(int64_t)t * E + e0 + q] = a;
-            }
+                for (int q = 0; q < 8; ++q) {
+                    float a = acc[i][q];
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+                    if (lane == 0 && i < nt && e0 + q < E) logits[(int64_t)(t0 + i) * E + e0 + q] = a;
+                }
         }
     }
 }
