@@ -296,6 +296,32 @@ def run_ours(args, cfg):
                    "exposed_ms": ms - comp_ms, "exposed_pct": 100.0 * (ms - comp_ms) / ms,
                    "definition": "T_layer - T_compute_only (same kernels, peer buffers replaced by local ones, no barriers), max over ranks"}
 
+    # ---- NCCL all-to-all + cuBLAS baseline (standard unfused EP), same shapes ----
+    nccl_ms = None
+    if not args.no_nccl_baseline and not injected and cfg.get("comm", "bf16") == "bf16":
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from nccl_moe_baseline import NcclMoEBaseline
+        g2 = torch.Generator(device="cuda").manual_seed(42)
+        bw1 = (torch.randn(el, 2 * f, h, device="cuda", generator=g2) / h ** 0.5).bfloat16()
+        bw2 = (torch.randn(el, h, f, device="cuda", generator=g2) / f ** 0.5).bfloat16()
+        base = NcclMoEBaseline(Tr, h, f, E, k, n, rank, bw1, bw2, wr)
+        for _ in range(2):
+            base.step(x, dy)
+        sync_all()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nb = max(3, args.steps // 5)
+        b0.record(stream)
+        for _ in range(nb):
+            base.step(x, dy)
+        b1.record(stream)
+        sync_all()
+        tb = torch.tensor([b0.elapsed_time(b1) / nb], device="cuda")
+        if world > 1:
+            dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        nccl_ms = float(tb.item())
+        del base, bw1, bw2
+        torch.cuda.empty_cache()
+
     # ---- per-phase device times (one instrumented step, same stream) ----
     L.enable_timing(True)
     phases = {}
@@ -413,6 +439,10 @@ def run_ours(args, cfg):
             "routing_rank0": routing_info,
             "memory_bound_ops": membw,
             "exposed_comm": exposed,
+            "nccl_a2a_cublas_baseline": None if nccl_ms is None else {
+                "ms_per_step": nccl_ms, "tokens_per_s": n * Tr / (nccl_ms / 1000.0),
+                "speedup_of_fused": nccl_ms / ms,
+                "what": "standard EP: NCCL all_to_all_single dispatch/combine + per-expert cuBLAS (torch) fwd+bwd"},
             "clocks": clk,
             "gpu_launches": int(launches),
             "gpu_launches_per_step": int(per_step_launches),
@@ -557,6 +587,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
+    ap.add_argument("--no-nccl-baseline", action="store_true")
     ap.add_argument("--trace", default=None, help="write the measured per-phase timeline (reference trace schema)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
