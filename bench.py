@@ -167,9 +167,15 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def layer_pad(L) -> int:
+    # mirrors the layer's tile choice (layer.cu): CTA pairs (256-row padding) at >= 900 rows/expert
+    return 256 if L.Tr * L.n * L.k / L.E >= 900 else 128
+
+
 def routing_probe_rows(L, rank, el):
     cnt = L.routing()["per_expert_counts"].cpu().tolist()[rank * el:(rank + 1) * el]
-    return int(sum((c + 255) // 256 * 256 for c in cnt))
+    p = layer_pad(L)
+    return int(sum((c + p - 1) // p * p for c in cnt))
 
 
 def run_ours(args, cfg):
@@ -408,7 +414,9 @@ def run_ours(args, cfg):
 
     rt = L.routing()
     cnt = rt["per_expert_counts"].cpu().tolist()[rank * el:(rank + 1) * el]
-    routing_info = {"local_rows": int(sum(cnt)), "padded_rows": int(sum((c + 255) // 256 * 256 for c in cnt)),
+    pad = layer_pad(L)
+    routing_info = {"local_rows": int(sum(cnt)), "padded_rows": int(sum((c + pad - 1) // pad * pad for c in cnt)),
+                    "row_padding": pad,
                     "max_expert_rows": int(max(cnt)), "min_expert_rows": int(min(cnt))}
     if rank == 0:
         peaks = load_peaks()

@@ -511,6 +511,13 @@ static __global__ void __launch_bounds__(256, 1) router_logits_smem_kernel(
     }
 }
 
+static __global__ void f32_to_bf16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const __nv_bfloat16 b = __float2bfloat16_rn(in[i]);
+        out[i] = *reinterpret_cast<const uint16_t*>(&b);
+    }
+}
+
 static __global__ void source_rank_kernel(int32_t* src, int T, int tokens_per_rank) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
         src[t] = t / tokens_per_rank;
