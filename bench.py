@@ -57,43 +57,65 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region via NVML
+    (every ~20 ms; falls back to nvidia-smi polling if NVML is unavailable)."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reason_bits)
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        hd = N.nvmlDeviceGetHandleByIndex(self.idx)
+        mx = N.nvmlDeviceGetMaxClockInfo(hd, N.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                self.samples.append((N.nvmlDeviceGetClockInfo(hd, N.NVML_CLOCK_SM), mx,
+                                     N.nvmlDeviceGetCurrentClocksEventReasons(hd)))
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def _run_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        bits = (0x8, 0x40, 0x20, 0x4)
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip().split(",")
+                rb = sum(b for b, v in zip(bits, out[2:]) if v.strip() == "Active")
+                self.samples.append((float(out[0]), float(out[1]), rb))
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
     def start(self):
-        def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([v.strip() for v in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-        self._t = threading.Thread(target=run, daemon=True)
+        try:
+            import pynvml  # noqa: F401
+            target = self._run_nvml
+        except Exception:
+            target = self._run_smi
+        self._t = threading.Thread(target=target, daemon=True)
         self._t.start()
 
     def stop(self):
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > i + 2 and s[i + 2] == "Active"})
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for s in self.samples for name, bit in self.REASONS if s[2] & bit})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "sm_max_mhz": max(s[1] for s in self.samples) if self.samples else None,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
 
 
 _CPU_STATE = {}
@@ -588,7 +610,7 @@ def run_attn(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
