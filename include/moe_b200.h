@@ -183,6 +183,9 @@ typedef struct {
     int32_t comm_format;     /* moe_comm_format */
     int32_t ep_pattern;      /* moe_ep_pattern */
     int32_t route_mode;      /* 0 = learned router (K1), 1 = injected experts/gates */
+    int32_t ffn_norm;        /* 1: RMSNorm (reference node ffn_norm, graph.cpp:267) fused ahead of
+                                the router and the dispatch; its backward follows the dx combine */
+    float norm_eps;
 } moe_layer_config;
 
 moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out);
@@ -195,7 +198,13 @@ void moe_layer_destroy(moe_layer* L);
 moe_status moe_layer_set_weights(moe_layer* L, const uint16_t* d_w1, const uint16_t* d_w2,
                                  const uint16_t* d_wr, moe_stream_t stream);
 
-/* Device pointer of the layer's symmetric input buffer [T_r, h] bf16. A
+/* ffn_norm = 1: RMSNorm weight gamma [h] fp32 (copied). */
+moe_status moe_layer_set_norm_weight(moe_layer* L, const float* d_gamma, moe_stream_t stream);
+/* ffn_norm = 1: d gamma [h] fp32 of the last backward (this rank's tokens), layer-owned. */
+const float* moe_layer_norm_grad(moe_layer* L);
+
+/* Device pointer of the layer's input buffer [T_r, h] bf16 (the pre-norm
+ * residual stream when ffn_norm = 1, else the symmetric buffer peers read). A
  * caller may write x there directly and pass NULL as d_x to forward. */
 uint16_t* moe_layer_input_buffer(moe_layer* L);
 

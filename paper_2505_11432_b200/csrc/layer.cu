@@ -55,6 +55,10 @@ struct moe_layer {
     // 256 rows); cg = 1 -> 128-row tiles for fine-grained experts where the
     // padding would cost more than the pair gains
     int cg = 2, pad = 256;
+    bool norm = false;         // ffn_norm fused ahead of router / dispatch
+    uint16_t* x_res = nullptr;  // pre-norm input [T_r, h]
+    uint16_t* dxn = nullptr;    // d(normed input) [T_r, h]
+    float *gamma = nullptr, *rstd = nullptr, *dgamma = nullptr, *dgamma_part = nullptr;
     bool gemm_router = false;  // router logits on the tensor cores (large E*h)
     bool gemm_router_wgrad = false;  // dWr = dlogits^T x on the tensor cores (E >= 128)
     uint16_t* dlogits_bf16 = nullptr;
@@ -369,6 +373,15 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->err, 1));
     TRY_ALLOC(dalloc(&L->epoch_dev, 1));
     TRY_ALLOC(dalloc(&L->router_rows, 1));
+    L->norm = c.ffn_norm != 0;
+    if (L->norm) {
+        TRY_ALLOC(dalloc(&L->x_res, Tr * h));
+        TRY_ALLOC(dalloc(&L->dxn, Tr * h));
+        TRY_ALLOC(dalloc(&L->gamma, h));
+        TRY_ALLOC(dalloc(&L->rstd, Tr));
+        TRY_ALLOC(dalloc(&L->dgamma, h));
+        TRY_ALLOC(dalloc(&L->dgamma_part, ((Tr + kRwChunk - 1) / kRwChunk) * h));
+    }
     TRY_ALLOC(dalloc(&L->dlogits_bf16, Tr * L->E));
     cudaMemset(L->err, 0, sizeof(int));
     cudaMemset(L->epoch_dev, 0, sizeof(uint32_t));
@@ -406,7 +419,8 @@ void moe_layer_destroy(moe_layer* L) {
                     L->expert_off, L->rows, L->gpad_rows, L->gpad_off, L->pad_tok, L->row_dst,
                     L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
                     L->dgate_part, L->dlogits, L->rw_part, L->ready, L->tab_remote, L->tab_local,
-                    L->err, L->epoch_dev, L->router_rows, L->dlogits_bf16};
+                    L->err, L->epoch_dev, L->router_rows, L->dlogits_bf16, L->x_res, L->dxn, L->gamma, L->rstd,
+                    L->dgamma, L->dgamma_part};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
@@ -427,7 +441,18 @@ moe_status moe_layer_set_weights(moe_layer* L, const uint16_t* d_w1, const uint1
     return MOE_OK;
 }
 
-uint16_t* moe_layer_input_buffer(moe_layer* L) { return L ? L->mine<uint16_t>(F_X) : nullptr; }
+uint16_t* moe_layer_input_buffer(moe_layer* L) {
+    return L ? (L->norm ? L->x_res : L->mine<uint16_t>(F_X)) : nullptr;
+}
+
+moe_status moe_layer_set_norm_weight(moe_layer* L, const float* d_gamma, moe_stream_t stream) {
+    MOE_CHECK_ARG(L && d_gamma, "null argument");
+    MOE_CHECK_ARG(L->norm, "layer created without ffn_norm");
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->gamma, d_gamma, L->h * 4, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return MOE_OK;
+}
+
+const float* moe_layer_norm_grad(moe_layer* L) { return L ? L->dgamma : nullptr; }
 
 moe_status moe_layer_set_routing(moe_layer* L, const int32_t* d_experts, const float* d_gates,
                                  moe_stream_t stream) {
@@ -450,8 +475,16 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     uint16_t* x_sym = L->mine<uint16_t>(F_X);
     for (int i = 0; i < PH_COUNT; ++i) L->ev_used[i] = false;
     L->mark(PH_ROUTE, s);
-    if (d_x && d_x != x_sym)
+    if (L->norm) {
+        // ffn_norm: the symmetric buffer peers pull from holds the NORMALISED tokens
+        if (d_x && d_x != L->x_res)
+            MOE_CUDA_TRY(cudaMemcpyAsync(L->x_res, d_x, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
+        rmsnorm_fwd_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->x_res, L->gamma, L->cfg.norm_eps, (int)Tr,
+                                                       (int)h, x_sym, L->rstd);
+        count_launch();
+    } else if (d_x && d_x != x_sym) {
         MOE_CUDA_TRY(cudaMemcpyAsync(x_sym, d_x, Tr * h * 2, cudaMemcpyDeviceToDevice, s));
+    }
     // K1 router (learned mode)
     if (L->cfg.route_mode == 0) {
         const size_t wbytes = (size_t)L->E * h * 4;  // fp32 in shared memory
@@ -655,18 +688,27 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     MOE_TRY(barrier(L, 3, s, 0));
     L->mark(PH_COMBINE_DX, s);
     const bool router = L->cfg.route_mode == 0;
+    uint16_t* dx_moe = L->norm ? L->dxn : d_dx;  // gradient w.r.t. the (normalised) layer input
     if (L->fp8)
         combine_reduce_kernel<true><<<kNumSMs * 4, 256, 0, s>>>(
             L->mine<uint8_t>(F_DSTAGE8), L->mine<float>(F_DSSC), drop_loc, (int)Tr, (int)k, (int)h,
-            d_dx, nullptr, router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
+            dx_moe, nullptr, router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
             router ? dgate_sym : nullptr, router ? L->wr : nullptr, router ? L->dlogits : nullptr,
             (int)L->E);
     else
         combine_reduce_kernel<false><<<kNumSMs * 4, 256, 0, s>>>(
-            L->mine<uint16_t>(F_DSTAGE), nullptr, drop_loc, (int)Tr, (int)k, (int)h, d_dx, nullptr,
+            L->mine<uint16_t>(F_DSTAGE), nullptr, drop_loc, (int)Tr, (int)k, (int)h, dx_moe, nullptr,
             router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr, router ? dgate_sym : nullptr,
             router ? L->wr : nullptr, router ? L->dlogits : nullptr, (int)L->E);
     count_launch();
+    if (L->norm) {
+        rmsnorm_bwd_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->x_res, L->gamma, L->rstd, L->dxn, (int)Tr, (int)h, d_dx);
+        const int nch = (int)((Tr + kRwChunk - 1) / kRwChunk);
+        rmsnorm_dgamma_partial_kernel<<<dim3((unsigned)((h + 255) / 256), nch), 256, 0, s>>>(
+            L->x_res, L->rstd, L->dxn, (int)Tr, (int)h, L->dgamma_part);
+        router_wgrad_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgamma_part, nch, 1, (int)h, L->dgamma);
+        count_launch(3);
+    }
     // dx is final here: callers may start its device->host copy while the
     // weight gradients below run (wgrad hidden under the dx transfer)
     if (dx_ready_event) MOE_CUDA_TRY(cudaEventRecord((cudaEvent_t)dx_ready_event, s));

@@ -511,6 +511,103 @@ static __global__ void __launch_bounds__(256, 1) router_logits_smem_kernel(
     }
 }
 
+// ffn_norm (graph.cpp:267): y = x * rsqrt(mean(x^2) + eps) * gamma, one warp
+// per token, rstd kept for the backward (the reference remats the norm in
+// backward, graph.cpp:355-359; here it is recomputed from x and rstd).
+static __global__ void rmsnorm_fwd_kernel(const uint16_t* __restrict__ x, const float* __restrict__ gamma,
+                                          float eps, int T, int h, uint16_t* __restrict__ y,
+                                          float* __restrict__ rstd) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int t = warp; t < T; t += nw) {
+        const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)t * h);
+        float ss = 0.0f;
+        for (int v = lane; v < h / 8; v += 32) {
+            const uint4 a = xr[v];
+            const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 p = unpack_bf16x2(w[q]);
+                ss += p.x * p.x + p.y * p.y;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        const float r = rsqrtf(ss / (float)h + eps);
+        if (lane == 0) rstd[t] = r;
+        uint4* yr = reinterpret_cast<uint4*>(y + (int64_t)t * h);
+        for (int v = lane; v < h / 8; v += 32) {
+            const uint4 a = xr[v];
+            const float4 g0 = reinterpret_cast<const float4*>(gamma)[2 * v];
+            const float4 g1 = reinterpret_cast<const float4*>(gamma)[2 * v + 1];
+            const float2 p0 = unpack_bf16x2(a.x), p1 = unpack_bf16x2(a.y), p2 = unpack_bf16x2(a.z), p3 = unpack_bf16x2(a.w);
+            yr[v] = make_uint4(pack_bf16x2(p0.x * r * g0.x, p0.y * r * g0.y), pack_bf16x2(p1.x * r * g0.z, p1.y * r * g0.w),
+                               pack_bf16x2(p2.x * r * g1.x, p2.y * r * g1.y), pack_bf16x2(p3.x * r * g1.z, p3.y * r * g1.w));
+        }
+    }
+}
+
+// RMSNorm backward: dx = rstd * (gamma*g - xhat * mean(xhat*gamma*g)), xhat = x*rstd
+static __global__ void rmsnorm_bwd_kernel(const uint16_t* __restrict__ x, const float* __restrict__ gamma,
+                                          const float* __restrict__ rstd, const uint16_t* __restrict__ g,
+                                          int T, int h, uint16_t* __restrict__ dx) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int t = warp; t < T; t += nw) {
+        const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)t * h);
+        const uint4* gr = reinterpret_cast<const uint4*>(g + (int64_t)t * h);
+        const float r = rstd[t];
+        float dot = 0.0f;
+        for (int v = lane; v < h / 8; v += 32) {
+            const uint4 a = xr[v], b = gr[v];
+            const float4 g0 = reinterpret_cast<const float4*>(gamma)[2 * v];
+            const float4 g1 = reinterpret_cast<const float4*>(gamma)[2 * v + 1];
+            const float gm[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 px = unpack_bf16x2(wa[q]), pg = unpack_bf16x2(wb[q]);
+                dot += px.x * r * gm[2 * q] * pg.x + px.y * r * gm[2 * q + 1] * pg.y;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+        const float mean = dot / (float)h;
+        uint4* dr = reinterpret_cast<uint4*>(dx + (int64_t)t * h);
+        for (int v = lane; v < h / 8; v += 32) {
+            const uint4 a = xr[v], b = gr[v];
+            const float4 g0 = reinterpret_cast<const float4*>(gamma)[2 * v];
+            const float4 g1 = reinterpret_cast<const float4*>(gamma)[2 * v + 1];
+            const float gm[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 px = unpack_bf16x2(wa[q]), pg = unpack_bf16x2(wb[q]);
+                o[q] = pack_bf16x2(r * (gm[2 * q] * pg.x - px.x * r * mean),
+                                   r * (gm[2 * q + 1] * pg.y - px.y * r * mean));
+            }
+            dr[v] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
+// d gamma partials: part[chunk, c] = sum over the chunk's tokens of g * xhat
+static __global__ void rmsnorm_dgamma_partial_kernel(const uint16_t* __restrict__ x, const float* __restrict__ rstd,
+                                                     const uint16_t* __restrict__ g, int T, int h,
+                                                     float* __restrict__ part) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t0 = blockIdx.y * kRwChunk, t1 = min(T, t0 + kRwChunk);
+    if (c >= h) return;
+    float acc = 0.0f;
+    for (int t = t0; t < t1; ++t) {
+        const float xv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(x)[(int64_t)t * h + c]);
+        const float gv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(g)[(int64_t)t * h + c]);
+        acc += gv * xv * rstd[t];
+    }
+    part[(int64_t)blockIdx.y * h + c] = acc;
+}
+
 static __global__ void f32_to_bf16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const __nv_bfloat16 b = __float2bfloat16_rn(in[i]);

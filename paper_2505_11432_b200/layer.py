@@ -19,7 +19,8 @@ class _Cfg(C.Structure):
     _fields_ = [("tokens_per_rank", C.c_int64), ("hidden", C.c_int64), ("ffn_hidden", C.c_int64),
                 ("num_experts", C.c_int64), ("top_k", C.c_int64), ("ep_size", C.c_int64),
                 ("rank", C.c_int64), ("capacity_factor", C.c_double), ("gate_order", C.c_int32),
-                ("comm_format", C.c_int32), ("ep_pattern", C.c_int32), ("route_mode", C.c_int32)]
+                ("comm_format", C.c_int32), ("ep_pattern", C.c_int32), ("route_mode", C.c_int32),
+                ("ffn_norm", C.c_int32), ("norm_eps", C.c_float)]
 
 
 class _RoutingView(C.Structure):
@@ -50,11 +51,12 @@ class MoELayer:
     def __init__(self, tokens_per_rank: int, hidden: int, ffn_hidden: int, num_experts: int,
                  top_k: int, ep_size: int = 1, rank: int = 0, capacity_factor: float = 0.0,
                  gate_order: str = "before_fc2_in", comm_format: str = "bf16",
-                 route_mode: str = "learned"):
+                 route_mode: str = "learned", ffn_norm: bool = False, norm_eps: float = 1e-6):
         cfg = _Cfg(tokens_per_rank, hidden, ffn_hidden, num_experts, top_k, ep_size, rank,
                    float(capacity_factor), GATE_ORDERS[gate_order],
                    {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}[comm_format], 0,
-                   {"learned": 0, "injected": 1}[route_mode])
+                   {"learned": 0, "injected": 1}[route_mode], int(bool(ffn_norm)), float(norm_eps))
+        self.norm = bool(ffn_norm)
         self.cfg = cfg
         self.Tr, self.h, self.f, self.E, self.k = tokens_per_rank, hidden, ffn_hidden, num_experts, top_k
         self.n, self.rank = ep_size, rank
@@ -86,6 +88,16 @@ class MoELayer:
         self._keep = (w1.contiguous(), w2.contiguous(), None if wr is None else wr.contiguous())
         check(lib().moe_layer_set_weights(self._h, ptr(self._keep[0]), ptr(self._keep[1]),
                                           ptr(self._keep[2]), stream_ptr(stream)))
+
+    def set_norm_weight(self, gamma: torch.Tensor, stream=None):
+        """ffn_norm weight [h] (fp32)."""
+        require_cuda(gamma)
+        self._gamma = gamma.float().contiguous()
+        check(lib().moe_layer_set_norm_weight(self._h, ptr(self._gamma), stream_ptr(stream)))
+
+    def norm_grad(self) -> torch.Tensor:
+        lib().moe_layer_norm_grad.restype = C.c_void_p
+        return _view(lib().moe_layer_norm_grad(self._h), (self.h,), torch.float32)
 
     def set_routing(self, experts: torch.Tensor, gates: torch.Tensor, stream=None):
         require_cuda(experts, gates)

@@ -131,3 +131,44 @@ def test_layer_gate_order_and_fp8_comm(gate_order, comm, tol):
                 dw2=rel(dw2.float().cpu().numpy(), ob["dw2"]), dwr=rel(dwr.cpu().numpy(), ob["dwr"]))
     print(gate_order, comm, errs)
     assert all(v < tol for v in errs.values()), errs
+
+
+def test_layer_with_fused_rmsnorm():
+    """ffn_norm (graph.cpp:267) ahead of router/dispatch: y = MoE(RMSNorm(x)).
+    Oracle: fp32 RMSNorm in numpy + the fp32 MoE oracle; backward chains the
+    oracle's d(normed input) through the RMSNorm backward."""
+    import pyoracle as P
+    from paper_2505_11432_b200.layer import MoELayer
+    T, h, f, E, k, eps = 256, 512, 512, 8, 2, 1e-6
+    g = torch.Generator().manual_seed(11)
+    x = (torch.randn(T, h, generator=g) * 2.0).bfloat16()
+    gamma = (1.0 + 0.1 * torch.randn(h, generator=g)).float()
+    w1 = (torch.randn(E, 2 * f, h, generator=g) / h ** 0.5).bfloat16()
+    w2 = (torch.randn(E, h, f, generator=g) / f ** 0.5).bfloat16()
+    wr = (torch.randn(E, h, generator=g) / h ** 0.5).bfloat16()
+    dy = (torch.randn(T, h, generator=g) * 0.1).bfloat16()
+    L = MoELayer(T, h, f, E, k, ffn_norm=True, norm_eps=eps)
+    L.set_weights(w1.cuda(), w2.cuda(), wr.cuda())
+    L.set_norm_weight(gamma.cuda())
+    y = L.forward(x.cuda())
+    dx, dw1, dw2, dwr = L.backward(dy.cuda())
+    torch.cuda.synchronize()
+    r = L.routing()
+    ex, gt, dr, lg = (r[q].cpu().numpy() for q in ("experts", "gates", "dropped", "logits"))
+    xf = x.float().numpy().astype(np.float64)
+    gm = gamma.numpy().astype(np.float64)
+    rstd = 1.0 / np.sqrt((xf ** 2).mean(1, keepdims=True) + eps)
+    xhat = xf * rstd
+    xn = (xhat * gm).astype(np.float32)
+    w1f, w2f, wrf = (t.float().numpy() for t in (w1, w2, wr))
+    oy = P.orc_moe_forward(xn, ex, gt, dr, w1f, w2f)
+    assert rel(y.float().cpu().numpy(), oy) < TOL
+    ob = P.orc_moe_backward(xn, dy.float().numpy(), ex, gt, lg, dr, w1f, w2f, wrf)
+    gn = ob["dx"].astype(np.float64)                 # d loss / d normed input
+    mean = (xhat * gm * gn).mean(1, keepdims=True)
+    odx = rstd * (gm * gn - xhat * mean)
+    odg = (gn * xhat).sum(0)
+    assert rel(dx.float().cpu().numpy(), odx) < TOL
+    assert rel(L.norm_grad().cpu().numpy(), odg) < TOL
+    assert rel(dw1.float().cpu().numpy(), ob["dw1"]) < TOL
+    assert rel(dwr.cpu().numpy(), ob["dwr"]) < TOL
