@@ -376,26 +376,40 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         uint16_t* d1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo;
         uint16_t* rf = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2;
         float dg = 0.0f;
+        // fc1_out loads for chunk c+1 are issued before chunk c is computed
+        uint4 va[4], vb[4];
+        {
+            const int j = n0 + c_lo;
+            const int ia = (j >> 7) * 256 + (j & 127);
+            load_rows32_issue(va, f1 + ia, lane);
+            load_rows32_issue(vb, f1 + ia + 128, lane);
+        }
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             const int j = n0 + c0;           // f column
             const int ia = (j >> 7) * 256 + (j & 127);
-            uint4 va[4], vb[4];
-            load_rows32_issue(va, f1 + ia, lane);        // coalesced fc1_out loads in flight
-            load_rows32_issue(vb, f1 + ia + 128, lane);  // while the accumulator is read
+            uint4 ca[4], cb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { ca[q] = va[q]; cb[q] = vb[q]; }
+            if (c0 + 32 < c_lo + HALF) {
+                const int jn = j + 32;
+                const int ian = (jn >> 7) * 256 + (jn & 127);
+                load_rows32_issue(va, f1 + ian, lane);
+                load_rows32_issue(vb, f1 + ian + 128, lane);
+            }
             uint32_t r[32];
             tmem_ld32(tbase + c0, r);
             tmem_ld_wait();
             uint32_t aw[16], bw[16];
-            load_rows32_finish(wst, va, aw, lane);
-            load_rows32_finish(wst, vb, bw, lane);
+            load_rows32_finish(wst, ca, aw, lane);
+            load_rows32_finish(wst, cb, bw, lane);
             uint32_t da[16], db[16], hf[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
                 const float2 a2 = unpack_bf16x2(aw[q]);
                 const float2 b2 = unpack_bf16x2(bw[q]);
                 const float d0 = __uint_as_float(r[2 * q]), d1v = __uint_as_float(r[2 * q + 1]);
-                const float s0 = 1.0f / (1.0f + __expf(-b2.x)), s1 = 1.0f / (1.0f + __expf(-b2.y));
+                const float s0 = __frcp_rn(1.0f + __expf(-b2.x)), s1 = __frcp_rn(1.0f + __expf(-b2.y));
                 const float si0 = b2.x * s0, si1 = b2.y * s1;
                 dg += d0 * a2.x * si0 + d1v * a2.y * si1;
                 da[q] = pack_bf16x2(d0 * g * si0, d1v * g * si1);
