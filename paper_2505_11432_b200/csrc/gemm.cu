@@ -13,11 +13,13 @@ static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, cons
     using Cfg = GemmCfg<BN, CG>;
     auto kern = grouped_gemm_kernel<BN, CG, A_MN, B_MN, KG, EPI, DISP>;
     constexpr int kThreads = Cfg::THREADS + (DISP ? 32 * Cfg::COMM_WARPS : 0);
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
+    static uint64_t attr_set = 0;  // per instantiation, one bit per device
+    int dev = 0;
+    MOE_CUDA_TRY(cudaGetDevice(&dev));
+    if (!(attr_set >> (dev & 63) & 1)) {
         MOE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           Cfg::SMEM_BYTES));
-        attr_set = true;
+        attr_set |= 1ull << (dev & 63);
     }
     if (CG == 1) {
         kern<<<grid, kThreads, Cfg::SMEM_BYTES, s>>>(ta, tb, a);
