@@ -471,6 +471,13 @@ def run_ours(args, cfg):
         fc1_ms = phases.get("fc1", float("nan"))
         achieved = fc1_flops / (fc1_ms / 1000.0) / 1e12
         total_flops = 3.0 * rows_local * 6.0 * h * f  # fwd+bwd expert FFN
+        traffic = None
+        try:  # DRAM bytes per fc1 launch from the committed ncu capture (same workload)
+            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+                if cfg["workload"].startswith("mixtral-8x7b-moe-layer-fwd+bwd") and n == 1:
+                    traffic = json.load(fh)["kernels"]["fc1"]["traffic_bytes"]
+        except Exception:
+            traffic = None
         line = {
             "metric": "moe_layer_fwd_bwd_tokens_per_s", "value": value, "unit": "tokens/s",
             "n_gpus": n, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -484,7 +491,7 @@ def run_ours(args, cfg):
                        "l2": "inputs larger than L2 (expert weights >= 2.8 GB/layer)"},
             "roofline": {"bound": "tensor", "kernel": "fc1 grouped GEMM (tcgen05) + fused SwiGLU",
                          "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
-                         "frac": achieved / peaks["bf16_sus"], "traffic": None,
+                         "frac": achieved / peaks["bf16_sus"], "traffic": traffic,
                          "peak_kind": f"bf16 sustained ({peaks['src']})",
                          "step_tflops": total_flops / (ms / 1000.0) / 1e12,
                          "step_frac": total_flops / (ms / 1000.0) / 1e12 / peaks["bf16_sus"]},
