@@ -191,7 +191,7 @@ def run_reference(args, cfg):
 
 def layer_pad(L) -> int:
     # mirrors the layer's tile choice (layer.cu): CTA pairs (256-row padding) at >= 900 rows/expert
-    return 256 if L.Tr * L.n * L.k / L.E >= 900 else 128
+    return 256 if L.Tr * L.n * L.k / L.E >= 256 else 128
 
 
 def routing_probe_rows(L, rank, el):
@@ -323,6 +323,12 @@ def run_ours(args, cfg):
         for _ in range(3):
             t_norm.append(window(False))
             t_comp.append(window(True))
+        # per-phase times in compute-only mode (where the step goes without NVLink)
+        L.enable_timing(True)
+        L.forward(None, y)
+        L.backward(dy, dx, dw1, dw2, dwr)
+        phases_co = L.phase_times()
+        L.enable_timing(False)
         L.set_compute_only(False)
         for _ in range(2):
             step()
@@ -331,6 +337,7 @@ def run_ours(args, cfg):
         exposed = {"t_layer_ms": tn, "t_compute_only_ms": tcm,
                    "exposed_ms": tn - tcm, "exposed_pct": 100.0 * (tn - tcm) / tn,
                    "windows_layer_ms": t_norm, "windows_compute_only_ms": t_comp,
+                   "phases_compute_only_ms": {kk: round(v, 4) for kk, v in phases_co.items()},
                    "definition": "median T_layer - median T_compute_only over 3 alternating windows (same "
                                  "kernels, peer buffers replaced by local ones, no barriers), max over ranks"}
 

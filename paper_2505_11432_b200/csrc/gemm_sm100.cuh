@@ -42,6 +42,9 @@ enum EpiKind : int {
 struct GemmArgs {
     int G;                      // number of groups (local experts)
     const int* group_rows;      // [G] padded rows per group (multiple of the tile height)
+    const int* group_k_rows;    // K-grouped only, optional: [G] real contraction rows per group
+                                // (the padding rows above them are zero, so the k loop stops at
+                                // the next 64-row block instead of the padded end)
     int N;                      // output columns
     int K;                      // M-grouped: contraction length; K-grouped: output rows M
     int b_group_stride;         // B coordinate offset per group (rows or K-rows)
@@ -132,7 +135,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
         // of B's (small) contraction panel from L2
         ti.n = li % n_tiles;
         ti.m = li / n_tiles;
-        ti.kblocks = a.group_rows[lo] >> 6;
+        ti.kblocks = a.group_k_rows ? (a.group_k_rows[lo] + 63) >> 6 : a.group_rows[lo] >> 6;
         ti.row0 = row_off[lo];   // contraction row offset
     }
     return ti;
@@ -440,52 +443,73 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid,
         if (i < 0) {
             for (int v = lane; v < nvec; v += 32) d[v] = make_uint4(0, 0, 0, 0);
         } else if (a.src_bufs8) {
-            // FP8 pull: 16 E4M3 codes per lane-step -> dequantise -> 2 x 16 B bf16
+            // FP8 pull: 16 E4M3 codes per lane-step -> dequantise -> 2 x 16 B bf16;
+            // up to 8 x 16 B loads in flight per lane (a 7168-wide row is 1 round)
             const int t = i / a.topk;
             const int src = t / a.tokens_per_rank;
             const int tl = t - src * a.tokens_per_rank;
             const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs8[src] + (int64_t)tl * K);
             const float* sc = a.src_scales[src] + (int64_t)tl * (K / a.src_scale_group);
             const float rs = a.row_scale ? a.row_scale[pp] : 1.0f;
-            for (int v = lane; v < K / 16; v += 32) {
-                const uint4 c = sp[v];
-                const float f = sc[(v * 16) / a.src_scale_group] * rs;
-                const uint32_t w[4] = {c.x, c.y, c.z, c.w};
-                uint32_t o[8];
+            const int n16 = K / 16;
+            constexpr int U8 = 16;
+            for (int v0 = lane; v0 < n16; v0 += 32 * U8) {
+                uint4 c[U8];
+                float f[U8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 lo = e4m3x2_to_f32x2((uint16_t)(w[q] & 0xffff));
-                    const float2 hi = e4m3x2_to_f32x2((uint16_t)(w[q] >> 16));
-                    o[2 * q] = pack_bf16x2(lo.x * f, lo.y * f);
-                    o[2 * q + 1] = pack_bf16x2(hi.x * f, hi.y * f);
+                for (int q = 0; q < U8; ++q) {
+                    const int v = v0 + 32 * q;
+                    if (v < n16) {
+                        c[q] = sp[v];
+                        f[q] = sc[(v * 16) / a.src_scale_group];
+                    }
                 }
-                d[2 * v] = make_uint4(o[0], o[1], o[2], o[3]);
-                d[2 * v + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+                for (int q = 0; q < U8; ++q) {
+                    const int v = v0 + 32 * q;
+                    if (v < n16) {
+                        const float fs = f[q] * rs;
+                        const uint32_t w[4] = {c[q].x, c[q].y, c[q].z, c[q].w};
+                        uint32_t o[8];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 lo = e4m3x2_to_f32x2((uint16_t)(w[e] & 0xffff));
+                            const float2 hi = e4m3x2_to_f32x2((uint16_t)(w[e] >> 16));
+                            o[2 * e] = pack_bf16x2(lo.x * fs, lo.y * fs);
+                            o[2 * e + 1] = pack_bf16x2(hi.x * fs, hi.y * fs);
+                        }
+                        d[2 * v] = make_uint4(o[0], o[1], o[2], o[3]);
+                        d[2 * v + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+                    }
+                }
             }
         } else {
+            // bf16 pull: 16 x 16 B loads in flight per lane before the stores
+            // (8 KB per warp; a 7168-wide row takes 2 rounds, 4096-wide 1)
             const int t = i / a.topk;
             const int src = t / a.tokens_per_rank;
             const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs[src] +
                                                              (int64_t)(t - src * a.tokens_per_rank) * K);
-            int v = lane;
-            if (a.row_scale) {
-                const float rs = a.row_scale[pp];
-                for (; v < nvec; v += 32) {
-                    const uint4 c = sp[v];
-                    const float2 p0 = unpack_bf16x2(c.x), p1 = unpack_bf16x2(c.y),
-                                 p2 = unpack_bf16x2(c.z), p3 = unpack_bf16x2(c.w);
-                    d[v] = make_uint4(pack_bf16x2(p0.x * rs, p0.y * rs), pack_bf16x2(p1.x * rs, p1.y * rs),
-                                      pack_bf16x2(p2.x * rs, p2.y * rs), pack_bf16x2(p3.x * rs, p3.y * rs));
+            const float rs = a.row_scale ? a.row_scale[pp] : 1.0f;
+            constexpr int U = 16;
+            for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+                uint4 r[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    if (v0 + 32 * q < nvec) r[q] = sp[v0 + 32 * q];
+                if (a.row_scale) {
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        const float2 p0 = unpack_bf16x2(r[q].x), p1 = unpack_bf16x2(r[q].y),
+                                     p2 = unpack_bf16x2(r[q].z), p3 = unpack_bf16x2(r[q].w);
+                        r[q] = make_uint4(pack_bf16x2(p0.x * rs, p0.y * rs), pack_bf16x2(p1.x * rs, p1.y * rs),
+                                          pack_bf16x2(p2.x * rs, p2.y * rs), pack_bf16x2(p3.x * rs, p3.y * rs));
+                    }
                 }
-            }
-            for (; v + 224 < nvec; v += 256) {
-                uint4 r[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) r[q] = sp[v + 32 * q];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) d[v + 32 * q] = r[q];
+                for (int q = 0; q < U; ++q)
+                    if (v0 + 32 * q < nvec) d[v0 + 32 * q] = r[q];
             }
-            for (; v < nvec; v += 32) d[v] = sp[v];
         }
         __syncwarp();
         if (lane == 0) {

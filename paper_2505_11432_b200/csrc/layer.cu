@@ -296,10 +296,11 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     L->el = L->E / L->n;
     L->first = L->rank * L->el;
     {
-        // CTA pairs gain ~12% per FLOP; padding to 256 instead of 128 rows costs
-        // ~64 rows per expert on average (measured 30% extra rows at 512 rows/expert)
+        // CTA pairs are 13-22% faster per FLOP at these shapes
+        // (scripts/perf_gemm_deepseek.py); padding to 256 instead of 128 rows
+        // costs ~64 more rows per expert on average: pairs win above ~256 rows/expert
         const double rows_per_expert = double(L->T * L->k) / double(L->E);
-        L->cg = rows_per_expert >= 900.0 ? 2 : 1;
+        L->cg = rows_per_expert >= 256.0 ? 2 : 1;
         if (const char* e = getenv("MOE_GEMM_CG")) L->cg = atoi(e) == 1 ? 1 : 2;
         L->pad = 128 * L->cg;
     }
@@ -719,6 +720,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.group_rows = L->gpad_rows;
         a.N = (int)f;
         a.K = (int)h;  // output rows per expert
+        a.group_k_rows = L->counts + L->first;
         a.out = d_dw2;
         a.ldo = f;
         MOE_TRY(gemm_launch(L->p_fc2_wgrad, a, s));
@@ -730,6 +732,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.group_rows = L->gpad_rows;
         a.N = (int)h;
         a.K = (int)(2 * f);
+        a.group_k_rows = L->counts + L->first;
         a.out = d_dw1;
         a.ldo = h;
         a.interleave_rows = 1;
