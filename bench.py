@@ -190,8 +190,9 @@ def run_reference(args, cfg):
 
 
 def layer_pad(L) -> int:
-    # mirrors the layer's tile choice (layer.cu): CTA pairs (256-row padding) at >= 900 rows/expert
-    return 256 if L.Tr * L.n * L.k / L.E >= 256 else 128
+    # expert segments are padded to 128 rows (layer.cu; CTA pairs run a segment's
+    # odd 128-row block as an M = 128 pair tile)
+    return 128
 
 
 def routing_probe_rows(L, rank, el):

@@ -271,7 +271,9 @@ moe_status moe_layer_set_fused_dispatch(moe_layer* L, int fused);
 /* Non-zero if a cross-GPU flag wait of this layer timed out (synchronous). */
 int moe_layer_error_flag(moe_layer* L);
 
-/* Generic grouped GEMM (reference OpKind::grouped_gemm): see gemm.h. */
+/* Generic grouped GEMM (reference OpKind::grouped_gemm): see gemm.h.
+ * M-grouped: every group's row count is a multiple of 128 (also with cta_pair: a
+ * group's last 128-row block then runs as an M = 128 CTA-pair tile). */
 moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b, void* d_d, int32_t groups,
                             const int32_t* d_group_rows, int64_t total_rows, int64_t M, int64_t N,
                             int64_t K, int32_t a_mn_major, int32_t b_mn_major, int32_t k_grouped,

@@ -118,7 +118,7 @@ moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_ran
     TRY(dalloc(&A->row_dst, A->s));
     TRY(dalloc(&A->rows_s, 1));
     TRY(dalloc(&A->rows_pad, 1));
-    TRY(dalloc(&A->ready, A->s / 256 + 1));
+    TRY(dalloc(&A->ready, A->s / 128 + 1));
     TRY(dalloc(&A->epoch_dev, 1));
     TRY(dalloc(&A->err, 1));
     cudaMemset(A->epoch_dev, 0, 4);
@@ -184,7 +184,7 @@ moe_status moe_attn_ag_gemm(moe_attn* A, const uint16_t* d_x_shard, uint16_t* d_
     if (d_x_shard && d_x_shard != xs)
         MOE_CUDA_TRY(cudaMemcpyAsync(xs, d_x_shard, A->sr * A->h * 2, cudaMemcpyDeviceToDevice, s));
     MOE_TRY(attn_barrier(A, 0, s));  // every shard is in place before peers pull it
-    MOE_CUDA_TRY(cudaMemsetAsync(A->ready, 0, (A->s / 256 + 1) * 4, s));
+    MOE_CUDA_TRY(cudaMemsetAsync(A->ready, 0, (A->s / 128 + 1) * 4, s));
     GemmArgs a{};
     a.G = 1;
     a.group_rows = A->rows_s;

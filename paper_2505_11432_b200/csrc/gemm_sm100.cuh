@@ -105,6 +105,7 @@ struct GemmCfg {
 // Tile-sequence helper shared by all roles.
 struct TileInfo {
     int g, m, n, kblocks, row0;
+    int half_tile;   // CG = 2, M-grouped: last tile of a group with only 128 rows -> M = 128 UMMA
 };
 
 template <int TILE_M, bool K_GROUPED>
@@ -119,8 +120,10 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
     TileInfo ti;
     ti.g = lo;
     int li = t - prefix[lo];
+    ti.half_tile = 0;
     if (!K_GROUPED) {
-        const int mt = a.group_rows[lo] / TILE_M;
+        const int rows = a.group_rows[lo];
+        const int mt = (rows + TILE_M - 1) / TILE_M;
         const int mc = (a.m_chunk > 0 && a.m_chunk < mt) ? a.m_chunk : mt;
         const int full = mc * n_tiles;
         const int c = li / full;
@@ -130,6 +133,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
         ti.m = c * mc + (r - ti.n * cm);
         ti.kblocks = (a.K + 63) / 64;
         ti.row0 = row_off[lo] + ti.m * TILE_M;
+        ti.half_tile = TILE_M == 256 && ti.m * TILE_M + TILE_M > rows;
     } else {
         // n fastest: a wave of tiles shares a few A panels and streams all
         // of B's (small) contraction panel from L2
@@ -249,7 +253,9 @@ __device__ __forceinline__ void load_rows32_finish(uint4* wst, const uint4 (&v)[
 template <int BN, int EPI, bool K_GROUPED>
 __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileInfo& ti,
                                               int64_t orow, uint32_t tbase, int c_lo,
-                                              int half, int n_tiles, uint4* wst) {
+                                              int half, int n_tiles, uint4* wst, int tshift) {
+    // accumulator column c of this warp's range lives in TMEM column c - tshift
+    // (tshift = 0 except for M = 128 pair tiles)
     const int lane = threadIdx.x & 31;
     const int n0 = ti.n * BN;
     constexpr int HALF = BN / 2;
@@ -273,7 +279,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             uint32_t r[32];
-            tmem_ld32(tbase + c0, r);
+            tmem_ld32(tbase + (c0 - tshift), r);
             tmem_ld_wait();
             if (n0 + c0 >= args.N) continue;   // warp-uniform
             if (EPI != EPI_STORE_F32) {
@@ -314,7 +320,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             uint32_t r[32];
-            tmem_ld32(tbase + c0, r);
+            tmem_ld32(tbase + (c0 - tshift), r);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(__uint_as_float(r[i])));
@@ -330,7 +336,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             uint32_t r[32];
-            tmem_ld32(tbase + c0, r);
+            tmem_ld32(tbase + (c0 - tshift), r);
             tmem_ld_wait();
             if (dst < 0) continue;
             uint32_t pk[8];
@@ -344,18 +350,20 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             *reinterpret_cast<uint4*>(codes + c0 + 16) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
     } else if constexpr (EPI == EPI_SWIGLU) {
-        // accumulator cols [0,BN/2) = a block, [BN/2,BN) = b block (W1 rows
-        // interleaved per BN/2 block at weight-pack time); this warp takes
-        // a/b pairs [half*BN/4, (half+1)*BN/4)
+        // W1 rows are packed per 128-row block as [a 64 | b 64] (pack_w1_kernel),
+        // so this warp's accumulator columns [c_lo, c_lo + 128) hold the a/b
+        // pairs of f-features ti.n * 128 + half * 64 + [0, 64). fc1_out is kept
+        // in this packed column order.
+        static_assert(BN == 256, "SwiGLU epilogue pairs a/b inside 128-column halves");
         const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
-        uint16_t* o1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
-        uint16_t* o2 = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2 + ti.n * HALF;
-        const int p_lo = half * (HALF / 2);
+        uint16_t* o1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0 + c_lo;
+        uint16_t* o2 = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2 + ti.n * HALF + half * (HALF / 2);
+        const uint32_t tb = tbase + (c_lo - tshift);
 #pragma unroll 1
-        for (int c0 = p_lo; c0 < p_lo + HALF / 2; c0 += 32) {
+        for (int c0 = 0; c0 < HALF / 2; c0 += 32) {
             uint32_t ra[32], rb[32];
-            tmem_ld32(tbase + c0, ra);
-            tmem_ld32(tbase + HALF + c0, rb);
+            tmem_ld32(tb + c0, ra);
+            tmem_ld32(tb + HALF / 2 + c0, rb);
             tmem_ld_wait();
             uint32_t pa[16], pb[16], ph[16];
 #pragma unroll
@@ -368,12 +376,12 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                 ph[q] = pack_bf16x2(a2.x * silu_f(b2.x) * g, a2.y * silu_f(b2.y) * g);
             }
             store_rows32(wst, pa, o1 + c0, lane);
-            store_rows32(wst, pb, o1 + HALF + c0, lane);
+            store_rows32(wst, pb, o1 + HALF / 2 + c0, lane);
             store_rows32(wst, ph, o2 + c0, lane);
         }
     } else if constexpr (EPI == EPI_SWIGLU_BWD) {
         // D = d fc2_in for f-columns [n0 + c_lo, +BN/2). fc1_out / dfc1 use the
-        // interleaved [a-block(128) | b-block(128)] layout.
+        // packed [a-block(64) | b-block(64)] column order of W1.
         const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
         const uint16_t* f1 = args.aux + orow * args.ld_aux;
         uint16_t* d1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo;
@@ -383,25 +391,25 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         uint4 va[4], vb[4];
         {
             const int j = n0 + c_lo;
-            const int ia = (j >> 7) * 256 + (j & 127);
+            const int ia = (j >> 6) * 128 + (j & 63);
             load_rows32_issue(va, f1 + ia, lane);
-            load_rows32_issue(vb, f1 + ia + 128, lane);
+            load_rows32_issue(vb, f1 + ia + 64, lane);
         }
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             const int j = n0 + c0;           // f column
-            const int ia = (j >> 7) * 256 + (j & 127);
+            const int ia = (j >> 6) * 128 + (j & 63);
             uint4 ca[4], cb[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) { ca[q] = va[q]; cb[q] = vb[q]; }
             if (c0 + 32 < c_lo + HALF) {
                 const int jn = j + 32;
-                const int ian = (jn >> 7) * 256 + (jn & 127);
+                const int ian = (jn >> 6) * 128 + (jn & 63);
                 load_rows32_issue(va, f1 + ian, lane);
-                load_rows32_issue(vb, f1 + ian + 128, lane);
+                load_rows32_issue(vb, f1 + ian + 64, lane);
             }
             uint32_t r[32];
-            tmem_ld32(tbase + c0, r);
+            tmem_ld32(tbase + (c0 - tshift), r);
             tmem_ld_wait();
             uint32_t aw[16], bw[16];
             load_rows32_finish(wst, ca, aw, lane);
@@ -421,7 +429,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                 hf[q] = pack_bf16x2(a2.x * si0 * g, a2.y * si1 * g);
             }
             store_rows32(wst, da, d1 + ia, lane);
-            store_rows32(wst, db, d1 + ia + 128, lane);
+            store_rows32(wst, db, d1 + ia + 64, lane);
             store_rows32(wst, hf, rf + j, lane);
         }
         if (args.row_part) args.row_part[orow * (2 * n_tiles) + ti.n * 2 + half] = dg;
@@ -514,7 +522,7 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid,
         __syncwarp();
         if (lane == 0) {
             fence_proxy_async_global();
-            red_release_gpu_add(&a.ready[pp / TILE_M], 1u);
+            red_release_gpu_add(&a.ready[pp / 128], 1u);
         }
     }
 }
@@ -555,7 +563,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             s_rowoff[g] = racc;
             const int rows = args.group_rows[g];
             racc += rows;
-            if (!K_GROUPED) acc += (rows / TILE_M) * n_tiles;
+            if (!K_GROUPED) acc += ((rows + TILE_M - 1) / TILE_M) * n_tiles;
             else acc += (args.K / TILE_M) * n_tiles;
         }
         prefix[G] = acc;
@@ -612,18 +620,23 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                     };
                     if (!K_GROUPED) {
                         if (DISPATCH && kb == 0) {
-                            // wait until this tile block's permuted rows have landed
-                            const uint32_t* rdy = &args.ready[ti.row0 / TILE_M];
+                            // wait until this tile's permuted rows (one counter per
+                            // 128-row block) have landed
+                            const uint32_t* rdy = &args.ready[ti.row0 / BM];
+                            const int nblk = ti.half_tile ? 1 : CG;
                             const uint64_t t0 = globaltimer();
-                            while (ld_acquire_gpu(rdy) < (uint32_t)TILE_M) {
-                                if (globaltimer() - t0 > 4000000000ull) {
-                                    atomicExch(args.err, 2);
-                                    break;
+                            for (int b = 0; b < nblk; ++b)
+                                while (ld_acquire_gpu(rdy + b) < (uint32_t)BM) {
+                                    if (globaltimer() - t0 > 4000000000ull) {
+                                        atomicExch(args.err, 2);
+                                        break;
+                                    }
                                 }
-                            }
                             fence_proxy_async_global();
                         }
-                        load(sa, &tmA, kb * 64, ti.row0 + arow);
+                        // half tile: each CTA of the pair takes 64 rows (the box's other
+                        // 64 rows are loaded but not read by the M = 128 UMMA)
+                        load(sa, &tmA, kb * 64, ti.row0 + (ti.half_tile ? (int)cta_rank * 64 : arow));
                         if (!B_MN) {
                             const int bbr = args.b_box_rows > 0 ? args.b_box_rows : BN_CTA;
                             for (int j = 0; j < BN_CTA; j += bbr)
@@ -651,7 +664,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
         if (lane == 0 && leader) {
-            constexpr uint32_t idesc = make_idesc(TILE_M, BN, 1, A_MN, B_MN);
+            constexpr uint32_t idesc_full = make_idesc(TILE_M, BN, 1, A_MN, B_MN);
+            constexpr uint32_t idesc_half = make_idesc(128, BN, 1, A_MN, B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -662,6 +676,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t idesc = ti.half_tile ? idesc_half : idesc_full;
                 for (int kb = 0; kb < ti.kblocks; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
@@ -706,10 +721,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             if (K_GROUPED) {
                 int mi = ti.m * TILE_M + (int)cta_rank * BM + r_in_cta;
                 if (args.interleave_rows) {
-                    const int blk = mi >> 8, w = mi & 255;
-                    mi = w < 128 ? blk * 128 + w : (args.K >> 1) + blk * 128 + (w - 128);
+                    const int blk = mi >> 7, w = mi & 127;
+                    mi = w < 64 ? blk * 64 + w : (args.K >> 1) + blk * 64 + (w - 64);
                 }
                 orow = (int64_t)ti.g * args.K + mi;
+            } else if (ti.half_tile) {
+                // M = 128 pair tile: each CTA holds 64 rows; TMEM lanes 0-63 carry
+                // accumulator columns [0, BN/2), lanes 64-127 columns [BN/2, BN),
+                // both in TMEM columns [0, BN/2) (scripts/probe_tmem_layout.cu)
+                orow = (int64_t)ti.row0 + (int)cta_rank * 64 + (quarter & 1) * 32 + lane;
             } else {
                 orow = (int64_t)ti.row0 + (int)cta_rank * BM + r_in_cta;
             }
@@ -730,8 +750,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-            epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, half * (BN / 2), half, n_tiles,
-                                              epi_stage + ew * 128);
+            if (!ti.half_tile) {
+                epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, half * (BN / 2), half, n_tiles,
+                                                  epi_stage + ew * 128, 0);
+            } else if (half == 0) {
+                // one warp per lane quarter covers the quarter's BN/2 columns
+                const int ch = quarter >> 1;
+                epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, ch * (BN / 2), ch, n_tiles,
+                                                  epi_stage + ew * 128, ch * (BN / 2));
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {

@@ -51,10 +51,10 @@ struct moe_layer {
     int64_t Tr = 0, T = 0, h = 0, f = 0, E = 0, k = 0, n = 1, rank = 0, el = 0, first = 0, Mp = 0;
     int dev = 0;
     bool fp8 = false, gate_after = false;
-    // GEMM tiling: cg = 2 -> CTA-pair 256-row tiles (expert segments padded to
-    // 256 rows); cg = 1 -> 128-row tiles for fine-grained experts where the
-    // padding would cost more than the pair gains
-    int cg = 2, pad = 256;
+    // GEMM tiling: cg = 2 -> CTA-pair 256-row tiles (a segment's odd 128-row
+    // block as an M = 128 pair tile); cg = 1 -> 128-row tiles for fine-grained
+    // experts. Expert segments are padded to 128 rows either way.
+    int cg = 2, pad = 128;
     bool norm = false;         // ffn_norm fused ahead of router / dispatch
     uint16_t* x_res = nullptr;  // pre-norm input [T_r, h]
     uint16_t* dxn = nullptr;    // d(normed input) [T_r, h]
@@ -302,7 +302,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
         const double rows_per_expert = double(L->T * L->k) / double(L->E);
         L->cg = rows_per_expert >= 256.0 ? 2 : 1;
         if (const char* e = getenv("MOE_GEMM_CG")) L->cg = atoi(e) == 1 ? 1 : 2;
-        L->pad = 128 * L->cg;
+        L->pad = 128;   // CTA pairs run a group's odd 128-row block as an M = 128 pair tile
     }
     L->Mp = L->T * L->k + L->el * L->pad;
     MOE_CHECK_ARG(L->T * L->k < (1ll << 27), "T*k must be < 2^27");

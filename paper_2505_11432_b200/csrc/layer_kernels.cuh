@@ -377,8 +377,8 @@ static __global__ void pack_w1_kernel(const uint16_t* __restrict__ w1, uint16_t*
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         const int e = (int)(r / (2 * f));
         const int j = (int)(r % (2 * f));
-        const int blk = j >> 8, w = j & 255;
-        const int src_j = w < 128 ? blk * 128 + w : f + blk * 128 + (w - 128);
+        const int blk = j >> 7, w = j & 127;   // [a 64 | b 64] per 128-row block
+        const int src_j = w < 64 ? blk * 64 + w : f + blk * 64 + (w - 64);
         const uint4* s = reinterpret_cast<const uint4*>(w1 + ((int64_t)e * 2 * f + src_j) * h);
         uint4* d = reinterpret_cast<uint4*>(w1p + r * h);
         for (int v = threadIdx.x; v < nvec; v += blockDim.x) d[v] = s[v];

@@ -13,7 +13,7 @@ def grouped_gemm(a: torch.Tensor, b: torch.Tensor, group_rows: torch.Tensor, *, 
                  out_dtype=torch.bfloat16, bn=256, cta_pair=False, out=None, stream=None) -> torch.Tensor:
     """M-grouped: a [rows, K] (K-major), b [G*N, K] (K-major) or [G*K, N]
     (MN-major) -> out [rows, N]; group g owns group_rows[g] rows (multiple
-    of 128, or of 256 with cta_pair). K-grouped: a [rows, M], b [rows, N] (both MN-major) ->
+    of 128; with cta_pair a trailing 128-row block runs as an M=128 pair tile). K-grouped: a [rows, M], b [rows, N] (both MN-major) ->
     out [G*M, N], out_g = a_g^T b_g."""
     require_cuda(a, b, group_rows)
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:

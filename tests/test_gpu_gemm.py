@@ -21,7 +21,7 @@ def test_m_grouped_kmajor(rows_per_group, N, K, bn, cta_pair):
     if cta_pair:
         if bn != 256:
             pytest.skip("CTA pairs use 256-wide tiles")
-        rows_per_group = [r * 2 for r in rows_per_group]   # multiples of 256
+        # 128-row multiples: odd counts end in an M=128 pair tile
     torch.manual_seed(1)
     G = len(rows_per_group)
     rows = sum(rows_per_group)
@@ -39,12 +39,10 @@ def test_m_grouped_kmajor(rows_per_group, N, K, bn, cta_pair):
             off += r
 
 
-@pytest.mark.parametrize("rows_per_group,N,K", [([128], 256, 64), ([256, 128], 512, 768)])
+@pytest.mark.parametrize("rows_per_group,N,K", [([128], 256, 64), ([256, 128], 512, 768), ([512, 384], 256, 512)])
 @pytest.mark.parametrize("cta_pair", [False, True])
 def test_m_grouped_b_mnmajor(rows_per_group, N, K, cta_pair):
     from paper_2505_11432_b200 import ops
-    if cta_pair:
-        rows_per_group = [r * 2 for r in rows_per_group]
     torch.manual_seed(2)
     G = len(rows_per_group)
     rows = sum(rows_per_group)
