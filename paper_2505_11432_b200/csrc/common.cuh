@@ -222,7 +222,16 @@ __host__ __device__ constexpr uint32_t make_idesc(uint32_t M, uint32_t N, uint32
 // ---------------------------------------------------------------------------
 // numeric helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float silu_f(float v) { return v / (1.0f + __expf(-v)); }
+// sigmoid via ex2.approx + rcp.approx (rcp of +inf is 0, so large negative
+// inputs give 0); the SwiGLU epilogues (fwd and bwd) share it, so the bwd
+// remat of fc2_in reproduces the forward values bit for bit
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sigmoid_f(float v) { return rcp_approx(1.0f + __expf(-v)); }
+__device__ __forceinline__ float silu_f(float v) { return v * sigmoid_f(v); }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

@@ -224,6 +224,30 @@ __device__ __forceinline__ void store_rows32(uint4* wst, const uint32_t (&pk)[16
     __syncwarp();
 }
 
+// Same, for a warp whose 32 rows are consecutive rows `stride` bytes apart
+// (every non-scatter epilogue): row addresses by arithmetic instead of shuffles.
+__device__ __forceinline__ void store_rows32_s(uint4* wst, const uint32_t (&pk)[16], void* row_ptr,
+                                               int64_t stride, int lane) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wst[xs_idx(lane, u)] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+    __syncwarp();
+    char* row0 = reinterpret_cast<char*>(row_ptr) - (int64_t)lane * stride;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int R = (lane >> 2) + 8 * i, c = lane & 3;
+        reinterpret_cast<uint4*>(row0 + (int64_t)R * stride)[c] = wst[xs_idx(R, c)];
+    }
+    __syncwarp();
+}
+__device__ __forceinline__ void load_rows32_issue_s(uint4 (&v)[4], const void* row_ptr, int64_t stride, int lane) {
+    const char* row0 = reinterpret_cast<const char*>(row_ptr) - (int64_t)lane * stride;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int R = (lane >> 2) + 8 * i, c = lane & 3;
+        v[i] = reinterpret_cast<const uint4*>(row0 + (int64_t)R * stride)[c];
+    }
+}
+
 // Issue the coalesced global loads of a 32 x 32 bf16 chunk (4 x 16 B per lane).
 __device__ __forceinline__ void load_rows32_issue(uint4 (&v)[4], const void* row_ptr, int lane) {
     const unsigned long long my = reinterpret_cast<unsigned long long>(row_ptr);
@@ -287,7 +311,8 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
 #pragma unroll
                 for (int q = 0; q < 16; ++q)
                     pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]) * gscale, __uint_as_float(r[2 * q + 1]) * gscale);
-                store_rows32(wst, pk, valid ? (void*)(obf + c0) : nullptr, lane);
+                if (EPI == EPI_SCATTER) store_rows32(wst, pk, valid ? (void*)(obf + c0) : nullptr, lane);
+                else store_rows32_s(wst, pk, obf + c0, args.ldo * 2, lane);
                 continue;
             }
             if (!valid) continue;
@@ -375,9 +400,9 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                 const float2 b2 = unpack_bf16x2(pb[q]);
                 ph[q] = pack_bf16x2(a2.x * silu_f(b2.x) * g, a2.y * silu_f(b2.y) * g);
             }
-            store_rows32(wst, pa, o1 + c0, lane);
-            store_rows32(wst, pb, o1 + HALF / 2 + c0, lane);
-            store_rows32(wst, ph, o2 + c0, lane);
+            store_rows32_s(wst, pa, o1 + c0, args.ldo * 2, lane);
+            store_rows32_s(wst, pb, o1 + HALF / 2 + c0, args.ldo * 2, lane);
+            store_rows32_s(wst, ph, o2 + c0, args.ldo2 * 2, lane);
         }
     } else if constexpr (EPI == EPI_SWIGLU_BWD) {
         // D = d fc2_in for f-columns [n0 + c_lo, +BN/2). fc1_out / dfc1 use the
@@ -392,8 +417,8 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         {
             const int j = n0 + c_lo;
             const int ia = (j >> 6) * 128 + (j & 63);
-            load_rows32_issue(va, f1 + ia, lane);
-            load_rows32_issue(vb, f1 + ia + 64, lane);
+            load_rows32_issue_s(va, f1 + ia, args.ld_aux * 2, lane);
+            load_rows32_issue_s(vb, f1 + ia + 64, args.ld_aux * 2, lane);
         }
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
@@ -405,8 +430,8 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             if (c0 + 32 < c_lo + HALF) {
                 const int jn = j + 32;
                 const int ian = (jn >> 6) * 128 + (jn & 63);
-                load_rows32_issue(va, f1 + ian, lane);
-                load_rows32_issue(vb, f1 + ian + 64, lane);
+                load_rows32_issue_s(va, f1 + ian, args.ld_aux * 2, lane);
+                load_rows32_issue_s(vb, f1 + ian + 64, args.ld_aux * 2, lane);
             }
             uint32_t r[32];
             tmem_ld32(tbase + (c0 - tshift), r);
@@ -420,7 +445,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                 const float2 a2 = unpack_bf16x2(aw[q]);
                 const float2 b2 = unpack_bf16x2(bw[q]);
                 const float d0 = __uint_as_float(r[2 * q]), d1v = __uint_as_float(r[2 * q + 1]);
-                const float s0 = __frcp_rn(1.0f + __expf(-b2.x)), s1 = __frcp_rn(1.0f + __expf(-b2.y));
+                const float s0 = sigmoid_f(b2.x), s1 = sigmoid_f(b2.y);
                 const float si0 = b2.x * s0, si1 = b2.y * s1;
                 dg += d0 * a2.x * si0 + d1v * a2.y * si1;
                 da[q] = pack_bf16x2(d0 * g * si0, d1v * g * si1);
@@ -428,9 +453,9 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                                     d1v * g * a2.y * s1 * (1.0f + b2.y * (1.0f - s1)));
                 hf[q] = pack_bf16x2(a2.x * si0 * g, a2.y * si1 * g);
             }
-            store_rows32(wst, da, d1 + ia, lane);
-            store_rows32(wst, db, d1 + ia + 64, lane);
-            store_rows32(wst, hf, rf + j, lane);
+            store_rows32_s(wst, da, d1 + ia, args.ldo * 2, lane);
+            store_rows32_s(wst, db, d1 + ia + 64, args.ldo * 2, lane);
+            store_rows32_s(wst, hf, rf + j, args.ldo2 * 2, lane);
         }
         if (args.row_part) args.row_part[orow * (2 * n_tiles) + ti.n * 2 + half] = dg;
     }
