@@ -43,6 +43,13 @@ CONFIGS = {
                              routing_fixture="tests/golden/routing_cfg5_zipf_nodrop_n8.npz"),
     # configs[3]: sequence-parallel attention QKV / out-proj, hidden 8192, seq 8192, GQA m=8
     "attn": dict(workload="sp-attention-qkv-ag-gemm+out-proj-gemm-rs", hidden=8192, seq=8192, gqa=8),
+    # §8f row 3: Ulysses SP projections (the paper's attention strategy) at the
+    # same cfg4 geometry
+    "ulysses": dict(workload="ulysses-sp-attention-qkv-gemm-a2a+a2a-out-proj-gemm", hidden=8192, seq=8192, gqa=8),
+    # §8f row 4: DP gradient sync with bf16 compression; gradient = one
+    # Mixtral expert's W1 + W2 (3 * 4096 * 14336 fp32), the per-rank expert
+    # parameters at EP = 8
+    "dp": dict(workload="dp-grad-sync-bf16-a2a-fp32-reduce", count=3 * 4096 * 14336),
 }
 
 
@@ -646,6 +653,212 @@ def run_attn(args, cfg):
         dist.destroy_process_group()
 
 
+def run_ulysses(args, cfg):
+    """§8f row 3: fused GEMM+A2A (QKV) and A2A+GEMM (out-proj) at SP = n, with
+    the cuBLAS + NCCL all_to_all baseline (incl. its layout permutes) timed in
+    the same run."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2505_11432_b200 import launch_count, launch_count_reset
+    from paper_2505_11432_b200.ulysses import UlyssesProjections
+    n, s_len, h, m = world, cfg["seq"], cfg["hidden"], cfg["gqa"]
+    nqkv = h * (m + 2) // m                    # h (1 + 2/m)  (graph.cpp:163-165)
+    sr, cpo, dh = s_len // n, nqkv // n, h // n
+    g = torch.Generator(device="cuda").manual_seed(3)
+    wqkv = (torch.randn(nqkv, h, device="cuda", generator=g) / h ** 0.5).bfloat16()
+    wout = (torch.randn(h, h, device="cuda", generator=g) / h ** 0.5).bfloat16()
+    g.manual_seed(11 + rank)
+    x = (torch.randn(sr, h, device="cuda", generator=g) * 0.5).bfloat16()
+    o = (torch.randn(s_len, dh, device="cuda", generator=g) * 0.5).bfloat16()
+    U = UlyssesProjections(s_len, h, nqkv, n, rank)
+    U.set_weights(wqkv, wout)
+    if n > 1:
+        U.connect()
+    U.attn_out.copy_(o)
+    y = torch.empty(sr, h, dtype=torch.bfloat16, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        U.qkv_a2a(x)
+        U.a2a_out_proj(None, y)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if n > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        sync_all()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
+        sync_all()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        if n > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    launch_count_reset()
+    step()
+    per_step = launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms = timed(step)
+    clk = clocks.stop()
+    ms_qkv = timed(lambda: U.qkv_a2a(x))
+    base = None
+    if not args.no_nccl_baseline:
+        qkv_loc = torch.empty(sr, nqkv, dtype=torch.bfloat16, device="cuda")
+        send = torch.empty(n, sr, cpo, dtype=torch.bfloat16, device="cuda")
+        recv = torch.empty(s_len, cpo, dtype=torch.bfloat16, device="cuda")
+        orecv = torch.empty(n, sr, dh, dtype=torch.bfloat16, device="cuda")
+        oseq = torch.empty(sr, h, dtype=torch.bfloat16, device="cuda")
+
+        def nccl_step():
+            torch.matmul(x, wqkv.T, out=qkv_loc)
+            send.copy_(qkv_loc.view(sr, n, cpo).transpose(0, 1))
+            if n > 1:
+                dist.all_to_all_single(recv, send.view(-1, cpo))
+                dist.all_to_all_single(orecv.view(-1, dh), o)
+            else:
+                recv.copy_(send.view(-1, cpo))
+                orecv.view(-1, dh).copy_(o)
+            oseq.view(sr, n, dh).copy_(orecv.transpose(0, 1))
+            torch.matmul(oseq, wout.T, out=y)
+        base = timed(nccl_step)
+    if rank == 0:
+        peaks = load_peaks()
+        flops = 2.0 * sr * h * nqkv + 2.0 * sr * h * h
+        link_bytes = (n - 1) / n * (s_len * cpo + s_len * dh) * 2 if n > 1 else 0.0   # into each rank
+        t_tensor = flops / (peaks["bf16"] * 1e12)
+        t_link = link_bytes / 770e9
+        line = {
+            "metric": "ulysses_attention_projection_pair_tokens_per_s", "value": s_len / (ms / 1000.0),
+            "unit": "tokens/s", "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "hidden": h, "seq": s_len, "gqa_ratio": m,
+                       "qkv_cols": nqkv, "parallelism": f"sp{n}"},
+            "roofline": {"bound": "nvlink" if t_link > t_tensor else "tensor",
+                         "target_ms": 1000 * max(t_tensor, t_link), "achieved_ms": ms,
+                         "frac": 1000 * max(t_tensor, t_link) / ms,
+                         "peak": "bf16 %.1f TF (measured burst), NVLink 770 GB/s/dir (measured ref.)" % peaks["bf16"]},
+            "qkv_gemm_a2a_ms": ms_qkv, "a2a_out_proj_gemm_ms": ms - ms_qkv,
+            "nccl_cublas_baseline_ms": base, "speedup_vs_nccl_baseline": (base / ms) if base else None,
+            "clocks": clk, "gpu_launches": per_step * args.steps, "launch_mode": "eager", "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    if n > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_dp(args, cfg):
+    """§8f row 4: compressed DP reduce-scatter (bf16 all-to-all + wide local
+    reduce, in place) and bf16 all-gather, beside NCCL's fp32 / bf16
+    reduce-scatter and bf16 all-gather of the same buffer."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2505_11432_b200 import launch_count, launch_count_reset
+    from paper_2505_11432_b200.dp import DpGradSync
+    n, count = world, cfg["count"]
+    S = count // n
+    D = DpGradSync(count, n, rank)
+    if n > 1:
+        D.connect()
+    g = torch.Generator(device="cuda").manual_seed(5 + rank)
+    D.grad.copy_(torch.randn(count, device="cuda", generator=g) * 1e-3)
+    upd = torch.randn(S, device="cuda", generator=g)
+    full = torch.empty(count, dtype=torch.bfloat16, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if n > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        sync_all()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
+        sync_all()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        if n > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    launch_count_reset()
+    D.reduce_scatter()
+    per_step = launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    # the buffer holds whatever the previous call left (finite floats): the
+    # timing does not depend on the values
+    ms_rs = timed(lambda: D.reduce_scatter())
+    clk = clocks.stop()
+    ms_ag = timed(lambda: D.all_gather_bf16(upd, full))
+    base = {}
+    if n > 1 and not args.no_nccl_baseline:
+        g32 = torch.randn(count, device="cuda", generator=g)
+        s32 = torch.empty(S, device="cuda")
+        g16, s16 = g32.bfloat16(), torch.empty(S, dtype=torch.bfloat16, device="cuda")
+        base["nccl_fp32_reduce_scatter_ms"] = timed(lambda: dist.reduce_scatter_tensor(s32, g32))
+        base["nccl_bf16_reduce_scatter_ms"] = timed(lambda: dist.reduce_scatter_tensor(s16, g16))
+        base["nccl_bf16_all_gather_ms"] = timed(lambda: dist.all_gather_into_tensor(full, s16))
+        del g32, g16
+    if rank == 0:
+        peaks = load_peaks()
+        wire = 2.0 * (n - 1) / n * count          # bf16 bytes into each rank per collective
+        # cast r+w, a2a reads, shard write (n = 1: one in-place read + write)
+        hbm = 8.0 * count if n == 1 else 4.0 * count + 2.0 * count + 2.0 * count + 4.0 * S
+        t_link = wire / 770e9
+        t_hbm = hbm / (peaks["hbm"] * 1e9)
+        bound = "nvlink" if t_link > t_hbm else "hbm"
+        line = {
+            "metric": "dp_grad_sync_fp32_bytes_per_s", "value": count * 4 / (ms_rs / 1000.0) / 1e9,
+            "unit": "GB/s (fp32 gradient bytes reduce-scattered per rank)", "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_rs, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 wire / fp64 reduce / fp32 out",
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "count": count, "dp": n, "shard": S,
+                       "inputs": "buffer > L2 (705 MB fp32)"},
+            "roofline": {"bound": bound, "target_ms": 1000 * max(t_link, t_hbm), "achieved_ms": ms_rs,
+                         "frac": 1000 * max(t_link, t_hbm) / ms_rs,
+                         "peak": "NVLink 770 GB/s/dir (measured ref.), HBM %.0f GB/s" % peaks["hbm"]},
+            "reduce_scatter_ms": ms_rs, "all_gather_bf16_ms": ms_ag, **base,
+            "clocks": clk, "gpu_launches": per_step * args.steps, "launch_mode": "eager", "e2e": None,
+        }
+        if "nccl_fp32_reduce_scatter_ms" in base:
+            line["speedup_vs_nccl_fp32_rs"] = base["nccl_fp32_reduce_scatter_ms"] / ms_rs
+        print(json.dumps(line), flush=True)
+    if n > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -663,6 +876,10 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.config == "ulysses":
+        run_ulysses(args, cfg)
+    elif args.config == "dp":
+        run_dp(args, cfg)
     elif args.config == "attn":
         run_attn(args, cfg)
     else:

@@ -335,6 +335,73 @@ moe_status moe_attn_ipc_export(moe_attn* A, void* h_blob);
 moe_status moe_attn_ipc_import(moe_attn* A, const void* h_blobs);
 int moe_attn_error_flag(moe_attn* A);
 
+/* ===================================================================== */
+/* Ulysses sequence-parallel attention projections (replicated weights)     */
+/* PAPER.md:150-160, 294-302; reference nodes qkv_proj -> a2a_qkv,          */
+/* a2a_attn_out -> out_proj (AttnStrategy::sp, graph.cpp:189-201)          */
+/* ===================================================================== */
+
+typedef struct moe_ulysses moe_ulysses; /* opaque */
+
+/* seq = full sequence length s (s/sp rows per rank), qkv_cols = h (1 + 2/m)
+ * for GQA ratio m (graph.cpp:163-165), ordered by owning rank: rank r's head
+ * group is columns [r * qkv_cols/sp, (r+1) * qkv_cols/sp). */
+moe_status moe_ulysses_create(int64_t seq, int64_t hidden, int64_t qkv_cols, int64_t sp_size,
+                              int64_t rank, moe_ulysses** out);
+void moe_ulysses_destroy(moe_ulysses* U);
+/* [s, qkv_cols/sp]: this rank's head group over the whole sequence, written by
+ * moe_ulysses_qkv_a2a (symmetric; peers store into it). */
+uint16_t* moe_ulysses_qkv_buffer(moe_ulysses* U);
+/* [s, hidden/sp]: this rank's attention output (its heads, whole sequence),
+ * read by every peer in moe_ulysses_a2a_out_proj. */
+uint16_t* moe_ulysses_attn_out_buffer(moe_ulysses* U);
+/* wqkv [qkv_cols, h], wout [h, h] (nn.Linear layout), replicated on every rank. */
+moe_status moe_ulysses_set_weights(moe_ulysses* U, const uint16_t* d_wqkv, const uint16_t* d_wout,
+                                   moe_stream_t stream);
+/* GEMM + A2A: qkv = x_shard[s/sp, h] . wqkv^T with every output tile stored
+ * into the rank owning its head group (fused in the GEMM epilogue). */
+moe_status moe_ulysses_qkv_a2a(moe_ulysses* U, const uint16_t* d_x_shard, moe_stream_t stream);
+/* A2A + GEMM: y_shard[s/sp, h] = o_seq . wout^T, where o_seq's rows are pulled
+ * head group by head group from every rank's attention output inside the
+ * GEMM. d_o_heads may be NULL if the output was written into the buffer. */
+moe_status moe_ulysses_a2a_out_proj(moe_ulysses* U, const uint16_t* d_o_heads, uint16_t* d_y_shard,
+                                    moe_stream_t stream);
+size_t moe_ulysses_ipc_handle_size(void);
+moe_status moe_ulysses_ipc_export(moe_ulysses* U, void* h_blob);
+moe_status moe_ulysses_ipc_import(moe_ulysses* U, const void* h_blobs);
+int moe_ulysses_error_flag(moe_ulysses* U);
+
+/* ===================================================================== */
+/* DP gradient sync with BF16 communication compression                    */
+/* PAPER.md:319-334; cost commcost.cpp:182-201 (dp_sync_time, compressed); */
+/* memory memmodel.cpp:112-114 (in-place operator: no transient peak)      */
+/* ===================================================================== */
+
+typedef struct moe_dp moe_dp; /* opaque */
+
+/* count fp32 gradient elements per rank (multiple of 4096 * dp_size). */
+moe_status moe_dp_create(int64_t count, int64_t dp_size, int64_t rank, moe_dp** out);
+void moe_dp_destroy(moe_dp* D);
+/* This rank's symmetric fp32 main-gradient buffer [count] (accumulate into it). */
+float* moe_dp_grad_buffer(moe_dp* D);
+/* Where moe_dp_reduce_scatter leaves this rank's reduced fp32 shard
+ * [count / dp_size] (inside the gradient buffer: its upper half, or the whole
+ * buffer when dp_size == 1). */
+float* moe_dp_shard(moe_dp* D);
+/* Compressed reduce-scatter, in place: cast the fp32 gradient to bf16 into the
+ * low half of its own buffer, all-to-all the bf16 shards over NVLink, sum each
+ * shard's dp_size pieces in rank order in binary64 and store fp32
+ * (= numerics::emulate_reduce(a2a_fp32) then one fp32 cast, numerics.cpp:172-192).
+ * The gradient buffer's contents are consumed. Collective: all ranks call. */
+moe_status moe_dp_reduce_scatter(moe_dp* D, moe_stream_t stream);
+/* bf16 all-gather of the updated shards: d_full[count] (bf16) receives every
+ * rank's d_shard[count / dp_size] (fp32, cast to bf16 once). Collective. */
+moe_status moe_dp_all_gather_bf16(moe_dp* D, const float* d_shard, uint16_t* d_full, moe_stream_t stream);
+size_t moe_dp_ipc_handle_size(void);
+moe_status moe_dp_ipc_export(moe_dp* D, void* h_blob);
+moe_status moe_dp_ipc_import(moe_dp* D, const void* h_blobs);
+int moe_dp_error_flag(moe_dp* D);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,6 +80,14 @@ struct GemmArgs {
     int src_scale_group;                // K (per-token) or 128 (grouped)
     const float* row_scale;             // optional extra per-permuted-row factor (gate)
     void* const* rank_scale_base;       // SCATTER_FP8: per destination rank scale base
+    // Ulysses sequence parallelism (attention projections)
+    int col_owner_cols;         // STORE_BF16 GEMM+A2A: output columns are owned in blocks of this
+                                // many by rank n0 / col_owner_cols; rows go to that rank's buffer
+                                // rank_base[owner] at row (owner_row0 + row), column n0 - base
+    int owner_row0;
+    int gather_cols;            // dispatch A2A+GEMM: A row = n_src pieces of gather_cols columns,
+                                // piece p = row (src_row0 + pp) of source p's [*, gather_cols]
+    int n_src, src_row0, src_rot;   // sources, row offset in each source, first source (rotation)
 };
 
 template <int BN, int CG>
@@ -296,7 +304,14 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                 obf = reinterpret_cast<uint16_t*>(args.rank_base[dst >> 27]) +
                       (int64_t)(dst & ((1 << 27) - 1)) * args.ldo + n0;
         } else if (EPI == EPI_STORE_BF16) {
-            obf = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
+            if (args.col_owner_cols > 0) {
+                // GEMM + all-to-all: this tile's columns belong to one rank's head group
+                const int owner = n0 / args.col_owner_cols;
+                obf = reinterpret_cast<uint16_t*>(args.rank_base[owner]) +
+                      (int64_t)(args.owner_row0 + orow) * args.ldo + (n0 - owner * args.col_owner_cols);
+            } else {
+                obf = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo + n0;
+            }
         } else {
             of32 = reinterpret_cast<float*>(args.out) + orow * args.ldo + n0;
         }
@@ -475,6 +490,26 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid,
         uint4* d = reinterpret_cast<uint4*>(a.a_dst + (int64_t)pp * K);
         if (i < 0) {
             for (int v = lane; v < nvec; v += 32) d[v] = make_uint4(0, 0, 0, 0);
+        } else if (a.gather_cols > 0) {
+            // all-to-all + GEMM: the row's column pieces come from every source,
+            // starting with this rank's own piece (rotation spreads the peers' load)
+            const int pv = a.gather_cols / 8;
+            for (int j = 0; j < a.n_src; ++j) {
+                const int src = (a.src_rot + j) % a.n_src;
+                const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs[src] +
+                                                                 (int64_t)(a.src_row0 + i) * a.gather_cols);
+                uint4* dp = d + src * pv;
+                constexpr int U = 8;
+                for (int v0 = lane; v0 < pv; v0 += 32 * U) {
+                    uint4 r[U];
+#pragma unroll
+                    for (int q = 0; q < U; ++q)
+                        if (v0 + 32 * q < pv) r[q] = sp[v0 + 32 * q];
+#pragma unroll
+                    for (int q = 0; q < U; ++q)
+                        if (v0 + 32 * q < pv) dp[v0 + 32 * q] = r[q];
+                }
+            }
         } else if (a.src_bufs8) {
             // FP8 pull: 16 E4M3 codes per lane-step -> dequantise -> 2 x 16 B bf16;
             // up to 8 x 16 B loads in flight per lane (a 7168-wide row is 1 round)
