@@ -466,11 +466,20 @@ def run_ours(args, cfg):
     nvlink = None
     if n > 1:
         osr = rt["out_source_rank"].cpu()
-        remote_rows = int((osr != rank).sum().item())
+        remote = osr != rank
+        remote_rows = int(remote.sum().item())
+        # dispatch dedup: a token with several experts on this rank is pulled once
+        # (layer.cu `dedup`; the gate-after backward pulls every row)
+        tok = rt["row_map_in"].cpu()[remote] // L.k
+        remote_tokens = int(torch.unique(tok).numel())
+        dedup = os.environ.get("MOE_DISPATCH_DEDUP") is not None and L.k > 1 and L.E // n > 1
+        pulled_fwd = remote_tokens if dedup else remote_rows
+        pulled_bwd = remote_rows if cfg.get("gate") == "after_fc2_out" else pulled_fwd
         bpe = 1 if cfg.get("comm", "bf16") == "fp8" else 2
-        fwd_b = remote_rows * h * bpe * 2            # dispatch x in + combine y out
-        bwd_b = remote_rows * h * bpe * 2            # dispatch dy in + combine dx out
-        nvlink = {"remote_rows": remote_rows, "bytes_per_step": fwd_b + bwd_b,
+        fwd_b = (pulled_fwd + remote_rows) * h * bpe  # dispatch x in + combine y out
+        bwd_b = (pulled_bwd + remote_rows) * h * bpe  # dispatch dy in + combine dx out
+        nvlink = {"remote_rows": remote_rows, "remote_tokens": remote_tokens, "rows_pulled": pulled_fwd,
+                  "bytes_per_step": fwd_b + bwd_b,
                   "link_GBps_if_spread_over_step": (fwd_b + bwd_b) / (ms / 1000.0) / 1e9,
                   "link_time_ms_at_770GBps": (fwd_b + bwd_b) / 770e9 * 1000.0,
                   "note": "bytes per direction per rank; overlapped inside fc1/fc2/fc2-dgrad/fc1-dgrad"}

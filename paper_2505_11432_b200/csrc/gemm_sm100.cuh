@@ -88,6 +88,10 @@ struct GemmArgs {
     int gather_cols;            // dispatch A2A+GEMM: A row = n_src pieces of gather_cols columns,
                                 // piece p = row (src_row0 + pp) of source p's [*, gather_cols]
     int n_src, src_row0, src_rot;   // sources, row offset in each source, first source (rotation)
+    // dispatch dedup (k > 1 experts of a token on this rank): row pp copies the
+    // already-landed row dup_src[pp] (< pp) locally instead of pulling it again
+    const int32_t* dup_src;     // [padded rows] earlier row of the same token, -1 = pull
+    uint32_t* row_done;         // [padded rows] set once a row has landed
 };
 
 template <int BN, int CG>
@@ -439,21 +443,12 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             const int j = n0 + c0;           // f column
             const int ia = (j >> 6) * 128 + (j & 63);
-            uint4 ca[4], cb[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) { ca[q] = va[q]; cb[q] = vb[q]; }
-            if (c0 + 32 < c_lo + HALF) {
-                const int jn = j + 32;
-                const int ian = (jn >> 6) * 128 + (jn & 63);
-                load_rows32_issue_s(va, f1 + ian, args.ld_aux * 2, lane);
-                load_rows32_issue_s(vb, f1 + ian + 64, args.ld_aux * 2, lane);
-            }
+            uint32_t aw[16], bw[16];
+            load_rows32_finish(wst, va, aw, lane);
+            load_rows32_finish(wst, vb, bw, lane);
             uint32_t r[32];
             tmem_ld32(tbase + (c0 - tshift), r);
             tmem_ld_wait();
-            uint32_t aw[16], bw[16];
-            load_rows32_finish(wst, ca, aw, lane);
-            load_rows32_finish(wst, cb, bw, lane);
             uint32_t da[16], db[16], hf[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -468,9 +463,16 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
                                     d1v * g * a2.y * s1 * (1.0f + b2.y * (1.0f - s1)));
                 hf[q] = pack_bf16x2(a2.x * si0 * g, a2.y * si1 * g);
             }
-            store_rows32_s(wst, da, d1 + ia, args.ldo * 2, lane);
-            store_rows32_s(wst, db, d1 + ia + 64, args.ldo * 2, lane);
-            store_rows32_s(wst, hf, rf + j, args.ldo2 * 2, lane);
+            // the next chunk's fc1_out loads fly while this chunk's rows are stored
+            if (c0 + 32 < c_lo + HALF) {
+                const int jn = j + 32;
+                const int ian = (jn >> 6) * 128 + (jn & 63);
+                load_rows32_issue(va, f1 + ian, lane);
+                load_rows32_issue(vb, f1 + ian + 64, lane);
+            }
+            store_rows32(wst, da, d1 + ia, lane);
+            store_rows32(wst, db, d1 + ia + 64, lane);
+            store_rows32(wst, hf, rf + j, lane);
         }
         if (args.row_part) args.row_part[orow * (2 * n_tiles) + ti.n * 2 + half] = dg;
     }
@@ -488,31 +490,11 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid,
     for (int pp = wid; pp < total; pp += nw) {
         const int i = a.pad_row_tok[pp];
         uint4* d = reinterpret_cast<uint4*>(a.a_dst + (int64_t)pp * K);
+        const int ds = (a.dup_src && i >= 0) ? a.dup_src[pp] : -1;
         if (i < 0) {
             for (int v = lane; v < nvec; v += 32) d[v] = make_uint4(0, 0, 0, 0);
-        } else if (a.gather_cols > 0) {
-            // all-to-all + GEMM: the row's column pieces come from every source,
-            // starting with this rank's own piece (rotation spreads the peers' load)
-            const int pv = a.gather_cols / 8;
-            for (int j = 0; j < a.n_src; ++j) {
-                const int src = (a.src_rot + j) % a.n_src;
-                const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs[src] +
-                                                                 (int64_t)(a.src_row0 + i) * a.gather_cols);
-                uint4* dp = d + src * pv;
-                constexpr int U = 8;
-                for (int v0 = lane; v0 < pv; v0 += 32 * U) {
-                    uint4 r[U];
-#pragma unroll
-                    for (int q = 0; q < U; ++q)
-                        if (v0 + 32 * q < pv) r[q] = sp[v0 + 32 * q];
-#pragma unroll
-                    for (int q = 0; q < U; ++q)
-                        if (v0 + 32 * q < pv) dp[v0 + 32 * q] = r[q];
-                }
-            }
-        } else if (a.src_bufs8) {
-            // FP8 pull: 16 E4M3 codes per lane-step -> dequantise -> 2 x 16 B bf16;
-            // up to 8 x 16 B loads in flight per lane (a 7168-wide row is 1 round)
+        } else if (a.src_bufs8 && ds < 0) {
+            // FP8 pull: 16 E4M3 codes per lane-step -> dequantise -> 2 x 16 B bf16
             const int t = i / a.topk;
             const int src = t / a.tokens_per_rank;
             const int tl = t - src * a.tokens_per_rank;
@@ -520,7 +502,7 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid,
             const float* sc = a.src_scales[src] + (int64_t)tl * (K / a.src_scale_group);
             const float rs = a.row_scale ? a.row_scale[pp] : 1.0f;
             const int n16 = K / 16;
-            constexpr int U8 = 16;
+            constexpr int U8 = 8;
             for (int v0 = lane; v0 < n16; v0 += 32 * U8) {
                 uint4 c[U8];
                 float f[U8];
@@ -552,35 +534,67 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid,
                 }
             }
         } else {
-            // bf16 pull: 16 x 16 B loads in flight per lane before the stores
-            // (8 KB per warp; a 7168-wide row takes 2 rounds, 4096-wide 1)
-            const int t = i / a.topk;
-            const int src = t / a.tokens_per_rank;
-            const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs[src] +
-                                                             (int64_t)(t - src * a.tokens_per_rank) * K);
-            const float rs = a.row_scale ? a.row_scale[pp] : 1.0f;
-            constexpr int U = 16;
-            for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
-                uint4 r[U];
-#pragma unroll
-                for (int q = 0; q < U; ++q)
-                    if (v0 + 32 * q < nvec) r[q] = sp[v0 + 32 * q];
-                if (a.row_scale) {
-#pragma unroll
-                    for (int q = 0; q < U; ++q) {
-                        const float2 p0 = unpack_bf16x2(r[q].x), p1 = unpack_bf16x2(r[q].y),
-                                     p2 = unpack_bf16x2(r[q].z), p3 = unpack_bf16x2(r[q].w);
-                        r[q] = make_uint4(pack_bf16x2(p0.x * rs, p0.y * rs), pack_bf16x2(p1.x * rs, p1.y * rs),
-                                          pack_bf16x2(p2.x * rs, p2.y * rs), pack_bf16x2(p3.x * rs, p3.y * rs));
+            // bf16 row copy in segments (one code path, 16 x 16 B loads in flight
+            // per lane = 8 KB per warp):
+            //   pull         1 segment: the token row on its owning rank (NVLink)
+            //   dedup        1 segment: the token's earlier row ds (< pp) in a_dst,
+            //                after it has landed (no wait cycle: ds < pp)
+            //   A2A gather   n_src segments of gather_cols columns, own rank first
+            const uint4* sp = nullptr;
+            float rs = 1.0f;
+            int nseg = 1, seg_vec = nvec;
+            if (ds >= 0) {
+                if (lane == 0) {
+                    const uint64_t t0 = globaltimer();
+                    while (ld_acquire_gpu(&a.row_done[ds]) == 0u) {
+                        if (globaltimer() - t0 > 4000000000ull) {
+                            atomicExch(a.err, 2);
+                            break;
+                        }
                     }
                 }
+                __syncwarp();
+                sp = reinterpret_cast<const uint4*>(a.a_dst + (int64_t)ds * K);
+            } else if (a.gather_cols > 0) {
+                nseg = a.n_src;
+                seg_vec = a.gather_cols / 8;
+            } else {
+                const int t = i / a.topk;
+                const int src = t / a.tokens_per_rank;
+                sp = reinterpret_cast<const uint4*>(a.src_bufs[src] + (int64_t)(t - src * a.tokens_per_rank) * K);
+                if (a.row_scale) rs = a.row_scale[pp];
+            }
+            for (int sg = 0; sg < nseg; ++sg) {
+                uint4* dp = d;
+                if (a.gather_cols > 0) {
+                    const int src = (a.src_rot + sg) % a.n_src;
+                    sp = reinterpret_cast<const uint4*>(a.src_bufs[src] + (int64_t)(a.src_row0 + i) * a.gather_cols);
+                    dp = d + src * seg_vec;
+                }
+                constexpr int U = 16;
+                for (int v0 = lane; v0 < seg_vec; v0 += 32 * U) {
+                    uint4 r[U];
 #pragma unroll
-                for (int q = 0; q < U; ++q)
-                    if (v0 + 32 * q < nvec) d[v0 + 32 * q] = r[q];
+                    for (int q = 0; q < U; ++q)
+                        if (v0 + 32 * q < seg_vec) r[q] = __ldcg(sp + v0 + 32 * q);
+                    if (rs != 1.0f) {
+#pragma unroll
+                        for (int q = 0; q < U; ++q) {
+                            const float2 p0 = unpack_bf16x2(r[q].x), p1 = unpack_bf16x2(r[q].y),
+                                         p2 = unpack_bf16x2(r[q].z), p3 = unpack_bf16x2(r[q].w);
+                            r[q] = make_uint4(pack_bf16x2(p0.x * rs, p0.y * rs), pack_bf16x2(p1.x * rs, p1.y * rs),
+                                              pack_bf16x2(p2.x * rs, p2.y * rs), pack_bf16x2(p3.x * rs, p3.y * rs));
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < U; ++q)
+                        if (v0 + 32 * q < seg_vec) dp[v0 + 32 * q] = r[q];
+                }
             }
         }
         __syncwarp();
         if (lane == 0) {
+            if (a.row_done && i >= 0) red_release_gpu_add(&a.row_done[pp], 1u);
             fence_proxy_async_global();
             red_release_gpu_add(&a.ready[pp / 128], 1u);
         }
@@ -810,15 +824,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-            if (!ti.half_tile) {
-                epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, half * (BN / 2), half, n_tiles,
-                                                  epi_stage + ew * 128, 0);
-            } else if (half == 0) {
-                // one warp per lane quarter covers the quarter's BN/2 columns
-                const int ch = quarter >> 1;
+            // half tile: one warp per lane quarter covers the quarter's BN/2 columns
+            const int ch = ti.half_tile ? (quarter >> 1) : half;
+            if (!ti.half_tile || half == 0)
                 epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, ch * (BN / 2), ch, n_tiles,
-                                                  epi_stage + ew * 128, ch * (BN / 2));
-            }
+                                                  epi_stage + ew * 128, ti.half_tile ? ch * (BN / 2) : 0);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {

@@ -90,6 +90,11 @@ struct moe_layer {
              *dfc1 = nullptr;
     float *dgate_part = nullptr, *dlogits = nullptr, *rw_part = nullptr;
     uint32_t* ready = nullptr;  // fused-dispatch arrival counters [Mp / L->pad]
+    // dispatch dedup when a token has several experts on this rank (k > 1,
+    // E/n > 1): later rows copy the first landed row instead of re-pulling it
+    bool dedup = false;
+    int32_t *first_row = nullptr, *dup_src = nullptr;
+    uint32_t* row_done = nullptr;
     bool fused_dispatch = true;
     int* err = nullptr;
     uint32_t* epoch_dev = nullptr;
@@ -219,6 +224,11 @@ void set_dispatch(moe_layer* L, GemmArgs& a, bool backward, uint16_t* dst) {
     a.topk = (int)L->k;
     a.tokens_per_rank = (int)L->Tr;
     a.err = L->err;
+    // the backward copy would carry the first row's gate (gate after fc2): pull instead
+    if (L->dedup && !(backward && L->gate_after)) {
+        a.dup_src = L->dup_src;
+        a.row_done = L->row_done;
+    }
     if (!backward) {
         a.src_bufs = L->tab<const uint16_t>(F_X);
         if (L->fp8) {
@@ -368,6 +378,9 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->dgate_part, Mp * (f / 256) * 2));
     TRY_ALLOC(dalloc(&L->dlogits, Tr * L->E));
     TRY_ALLOC(dalloc(&L->ready, Mp / L->pad + 1));
+    TRY_ALLOC(dalloc(&L->first_row, L->T));
+    TRY_ALLOC(dalloc(&L->dup_src, Mp));
+    TRY_ALLOC(dalloc(&L->row_done, Mp));
     TRY_ALLOC(dalloc(&L->rw_part, ((Tr + kRwChunk - 1) / kRwChunk) * L->E * h));
     TRY_ALLOC(dalloc(&L->tab_remote, F_COUNT * L->n));
     TRY_ALLOC(dalloc(&L->tab_local, F_COUNT * L->n));
@@ -389,6 +402,10 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     // the unfused (reference-structure) dispatch path is kept for A/B runs;
     // gate-after-fc2 backward needs the fused path's row scaling
     L->fused_dispatch = getenv("MOE_UNFUSED_DISPATCH") == nullptr || L->gate_after || L->fp8;
+    // off by default: at EP = 4 the pulls are hidden under fc1 / fc2-dgrad and the
+    // wait for the first row costs more than the NVLink bytes it saves (A/B in
+    // DESIGN.md); MOE_DISPATCH_DEDUP=1 turns it on for link-bound configurations
+    L->dedup = L->n > 1 && L->k > 1 && L->el > 1 && getenv("MOE_DISPATCH_DEDUP") != nullptr;
     // zero the permuted buffers once so never-written rows are finite
     cudaMemset(L->x_perm, 0, Mp * h * 2);
     cudaMemset(L->dy_perm, 0, Mp * h * 2);
@@ -419,7 +436,8 @@ void moe_layer_destroy(moe_layer* L) {
                     L->dropped, L->perm_ws, L->row_map_in, L->out_expert, L->out_src, L->counts,
                     L->expert_off, L->rows, L->gpad_rows, L->gpad_off, L->pad_tok, L->row_dst,
                     L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
-                    L->dgate_part, L->dlogits, L->rw_part, L->ready, L->tab_remote, L->tab_local,
+                    L->dgate_part, L->dlogits, L->rw_part, L->ready, L->first_row, L->dup_src, L->row_done,
+                    L->tab_remote, L->tab_local,
                     L->err, L->epoch_dev, L->router_rows, L->dlogits_bf16, L->x_res, L->dxn, L->gamma, L->rstd,
                     L->dgamma, L->dgamma_part};
     for (void* b : bufs)
@@ -540,10 +558,17 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
                                                  L->pad_tok, L->mine<float>(F_GT), (int)k, (int)Tr,
                                                  L->row_gate, L->row_dst);
     count_launch();
+    if (L->dedup) {
+        MOE_CUDA_TRY(cudaMemsetAsync(L->first_row, 0x7f, L->T * 4, s));
+        first_row_kernel<<<kNumSMs * 2, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, L->first_row);
+        dup_src_kernel<<<kNumSMs * 2, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, L->first_row, L->dup_src);
+        count_launch(2);
+    }
     // dispatch: AG + local scatter (rows pulled from the owning rank)
     L->mark(PH_DISPATCH, s);
     if (L->fused_dispatch) {
         MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 1) * 4, s));
+        if (L->dedup) MOE_CUDA_TRY(cudaMemsetAsync(L->row_done, 0, L->Mp * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
                                                          (int)h, L->tab<const uint16_t>(F_X), L->x_perm);
@@ -638,6 +663,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     // AG(dy) + scatter into permuted order (fused into the fc2 dgrad GEMM)
     if (L->fused_dispatch) {
         MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 1) * 4, s));
+        if (L->dedup && !L->gate_after) MOE_CUDA_TRY(cudaMemsetAsync(L->row_done, 0, L->Mp * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
                                                          (int)h, L->tab<const uint16_t>(F_DY), L->dy_perm);

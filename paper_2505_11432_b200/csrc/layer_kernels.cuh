@@ -40,6 +40,27 @@ static __global__ void row_info_kernel(const int32_t* __restrict__ group_pad_off
     }
 }
 
+// Dispatch dedup: the first padded row of every token on this rank
+// (first_row pre-filled with 0x7f7f7f7f), then every later row of the same
+// token points at it (its k experts on one rank need the token row once).
+static __global__ void first_row_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad, int k,
+                                        int32_t* __restrict__ first_row) {
+    const int total = *nrows_pad;
+    for (int pp = blockIdx.x * blockDim.x + threadIdx.x; pp < total; pp += gridDim.x * blockDim.x) {
+        const int i = pad_row_tok[pp];
+        if (i >= 0) atomicMin(&first_row[i / k], pp);
+    }
+}
+static __global__ void dup_src_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad, int k,
+                                      const int32_t* __restrict__ first_row, int32_t* __restrict__ dup_src) {
+    const int total = *nrows_pad;
+    for (int pp = blockIdx.x * blockDim.x + threadIdx.x; pp < total; pp += gridDim.x * blockDim.x) {
+        const int i = pad_row_tok[pp];
+        const int f = i >= 0 ? first_row[i / k] : pp;
+        dup_src[pp] = f != pp ? f : -1;
+    }
+}
+
 // Dispatch: dst[pp, :] = src_rank_buffer[t_local, :] for real rows, 0 for
 // pads (AG + local scatter fused: rows are pulled straight from the owning
 // rank's buffer over NVLink into permuted order).
