@@ -289,7 +289,8 @@ __device__ __forceinline__ void load_rows32_finish(uint4* wst, const uint4 (&v)[
 template <int BN, int EPI, bool K_GROUPED>
 __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileInfo& ti,
                                               int64_t orow, uint32_t tbase, int c_lo,
-                                              int half, int n_tiles, uint4* wst, int tshift) {
+                                              int half, int n_tiles, uint4* wst, int tshift,
+                                              uint4 (&va)[4], uint4 (&vb)[4]) {
     // accumulator column c of this warp's range lives in TMEM column c - tshift
     // (tshift = 0 except for M = 128 pair tiles)
     const int lane = threadIdx.x & 31;
@@ -431,14 +432,8 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         uint16_t* d1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo;
         uint16_t* rf = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2;
         float dg = 0.0f;
-        // fc1_out loads for chunk c+1 are issued before chunk c is computed
-        uint4 va[4], vb[4];
-        {
-            const int j = n0 + c_lo;
-            const int ia = (j >> 6) * 128 + (j & 63);
-            load_rows32_issue_s(va, f1 + ia, args.ld_aux * 2, lane);
-            load_rows32_issue_s(vb, f1 + ia + 64, args.ld_aux * 2, lane);
-        }
+        // va / vb: the first chunk's fc1_out rows, issued by the caller before it
+        // waited for the accumulator; chunk c+1's loads fly during chunk c's stores
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             const int j = n0 + c0;           // f column
@@ -821,14 +816,27 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                 }
                 continue;
             }
+            // half tile: one warp per lane quarter covers the quarter's BN/2 columns
+            const int ch = ti.half_tile ? (quarter >> 1) : half;
+            const bool active = !ti.half_tile || half == 0;
+            uint4 va[4], vb[4];
+            if constexpr (EPI == EPI_SWIGLU_BWD) {
+                // the epilogue's own global operand (fc1_out) does not depend on the
+                // accumulator: put the first chunk in flight before waiting for it
+                if (active) {
+                    const int j = n0 + ch * (BN / 2);
+                    const int ia = (j >> 6) * 128 + (j & 63);
+                    const uint16_t* f1 = args.aux + orow * args.ld_aux;
+                    load_rows32_issue(va, f1 + ia, lane);
+                    load_rows32_issue(vb, f1 + ia + 64, lane);
+                }
+            }
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-            // half tile: one warp per lane quarter covers the quarter's BN/2 columns
-            const int ch = ti.half_tile ? (quarter >> 1) : half;
-            if (!ti.half_tile || half == 0)
+            if (active)
                 epilogue_rows<BN, EPI, K_GROUPED>(args, ti, orow, tbase, ch * (BN / 2), ch, n_tiles,
-                                                  epi_stage + ew * 128, ti.half_tile ? ch * (BN / 2) : 0);
+                                                  epi_stage + ew * 128, ti.half_tile ? ch * (BN / 2) : 0, va, vb);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
