@@ -151,6 +151,9 @@ def cpu_reference_step(cfg, sample_tokens, seed=0, with_dense=True):
     x = (rng.standard_normal((S, h), dtype=np.float32) * np.float32(0.5))
     dy = (rng.standard_normal((S, h), dtype=np.float32) * np.float32(0.1))
     kind = "reference" if P.ref_available() else "port"
+    # all host cores (torchrun exports OMP_NUM_THREADS=1 to every rank)
+    P.oracle_lib().orc_set_threads(os.cpu_count() or 1)
+    threads = int(P.oracle_lib().orc_get_threads())
     t0 = time.perf_counter()
     logits, ex, gates = P.orc_router_topk(x, wr, k)
     src = np.zeros(S, np.int32)
@@ -165,7 +168,7 @@ def cpu_reference_step(cfg, sample_tokens, seed=0, with_dense=True):
         P.orc_moe_forward(x, ex, gates, dr, w1, w2)
         P.orc_moe_backward(x, dy, ex, gates, logits, dr, w1, w2, wr)
     dt = time.perf_counter() - t0
-    return dt, kind, os.cpu_count()
+    return dt, kind, threads
 
 
 def run_reference(args, cfg):
@@ -502,6 +505,29 @@ def run_ours(args, cfg):
                     traffic = json.load(fh)["kernels"]["fc1"]["traffic_bytes"]
         except Exception:
             traffic = None
+        # fc1's bound: tensor time vs HBM time of its algorithmic bytes (this rank's
+        # W1 once, the permuted rows in, fc1_out + fc2_in out). Fine-grained experts
+        # on few GPUs (DeepSeek shape at n = 1: 15 GB of W1) are HBM-bound.
+        fc1_bytes = el * 2 * f * h * 2 + rows_local * h * 2 + rows_local * 3 * f * 2
+        t_tc, t_hbm = fc1_flops / (peaks["bf16_sus"] * 1e12), fc1_bytes / (peaks["hbm"] * 1e9)
+        # step: expert FLOPs vs weights read twice (fwd, dgrad) + weight grads written
+        # + activations (x, fc1_out, fc2_in, dy, dfc1 streams)
+        step_bytes = 3 * el * 3 * f * h * 2 + rows_local * (4 * h + 8 * f) * 2
+        st_tc, st_hbm = total_flops / (peaks["bf16_sus"] * 1e12), step_bytes / (peaks["hbm"] * 1e9)
+        if t_hbm > t_tc:
+            gbs = fc1_bytes / (fc1_ms / 1000.0) / 1e9
+            roof = {"bound": "hbm", "kernel": "fc1 grouped GEMM (tcgen05) + fused SwiGLU",
+                    "achieved": gbs, "peak": peaks["hbm"], "unit": "GB/s", "frac": gbs / peaks["hbm"],
+                    "traffic": traffic, "algorithmic_bytes": fc1_bytes, "peak_kind": f"HBM ({peaks['src']})"}
+        else:
+            roof = {"bound": "tensor", "kernel": "fc1 grouped GEMM (tcgen05) + fused SwiGLU",
+                    "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
+                    "frac": achieved / peaks["bf16_sus"], "traffic": traffic,
+                    "algorithmic_bytes": fc1_bytes, "peak_kind": f"bf16 sustained ({peaks['src']})"}
+        roof.update({"step_bound": "hbm" if st_hbm > st_tc else "tensor",
+                     "step_roofline_ms": 1000 * max(st_tc, st_hbm),
+                     "step_frac": 1000 * max(st_tc, st_hbm) / ms,
+                     "step_tflops": total_flops / (ms / 1000.0) / 1e12})
         line = {
             "metric": "moe_layer_fwd_bwd_tokens_per_s", "value": value, "unit": "tokens/s",
             "n_gpus": n, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -513,12 +539,7 @@ def run_ours(args, cfg):
                        "parallelism": f"ep{n}", "comm_format": cfg.get("comm", "bf16"),
                        "gate_order": cfg.get("gate", "before_fc2_in"),
                        "l2": "inputs larger than L2 (expert weights >= 2.8 GB/layer)"},
-            "roofline": {"bound": "tensor", "kernel": "fc1 grouped GEMM (tcgen05) + fused SwiGLU",
-                         "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
-                         "frac": achieved / peaks["bf16_sus"], "traffic": traffic,
-                         "peak_kind": f"bf16 sustained ({peaks['src']})",
-                         "step_tflops": total_flops / (ms / 1000.0) / 1e12,
-                         "step_frac": total_flops / (ms / 1000.0) / 1e12 / peaks["bf16_sus"]},
+            "roofline": roof,
             "phases_ms": {kk: round(v, 4) for kk, v in phases.items()},
             "routing_rank0": routing_info,
             "memory_bound_ops": membw,

@@ -27,6 +27,11 @@
  * the full per-group slot counts; scan t = T-1..0; a token whose groups
  * include ANY group with load > capacity is dropped whole and decrements
  * all of its groups. Group of expert e = e / (E/n) (routing.cpp:44-47). */
+/* Thread count of the dense fp32 parts (the host process may inherit
+ * OMP_NUM_THREADS=1 from a launcher; the CPU baseline sets it explicitly). */
+void orc_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
+int orc_get_threads(void) { return omp_get_max_threads(); }
+
 int orc_capacity_drop(int64_t T, int64_t E, int64_t k, int64_t n_groups, double cf,
                       const int32_t* experts, uint8_t* dropped) {
     if (T < 0 || E < 1 || k < 1 || n_groups < 1 || E % n_groups != 0 || !(cf > 0.0)) return -2;
