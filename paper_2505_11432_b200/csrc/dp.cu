@@ -136,12 +136,26 @@ __global__ void dp_cast_shard_kernel(const float* __restrict__ src, uint16_t* __
     }
 }
 
-// out[p*S + i] = peer_p[p*S + i] (bf16), all peers, 16 B per thread-step
-__global__ void dp_gather_kernel(const uint16_t* const* bufs, int n, int64_t S, uint16_t* __restrict__ out) {
+// out[p*S + i] = peer_p[p*S + i] (bf16), all peers; 8 independent 16 B loads
+// in flight per thread (peer reads over NVLink are latency-bound otherwise),
+// peers visited starting from this rank so the links are loaded evenly
+__global__ void dp_gather_kernel(const uint16_t* const* bufs, int n, int rank, int64_t S, uint16_t* __restrict__ out) {
+    constexpr int U = 8;
     const int64_t nv = S / 8;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv * n; v += (int64_t)gridDim.x * blockDim.x) {
-        const int p = (int)(v / nv);
-        reinterpret_cast<uint4*>(out)[v] = reinterpret_cast<const uint4*>(bufs[p])[v];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int j = 0; j < n; ++j) {
+        const int p = (rank + j) % n;
+        const uint4* src = reinterpret_cast<const uint4*>(bufs[p]) + p * nv;
+        uint4* dst = reinterpret_cast<uint4*>(out) + p * nv;
+        for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nv; v0 += stride * U) {
+            uint4 r[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (v0 + q * stride < nv) r[q] = src[v0 + q * stride];
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (v0 + q * stride < nv) dst[v0 + q * stride] = r[q];
+        }
     }
 }
 
@@ -260,8 +274,8 @@ moe_status moe_dp_all_gather_bf16(moe_dp* D, const float* d_shard, uint16_t* d_f
     dp_cast_shard_kernel<<<grid_for(D->shard / 4), 256, 0, s>>>(d_shard, lo + D->rank * D->shard, D->shard);
     count_launch();
     MOE_TRY(dp_barrier(D, 2, s));
-    dp_gather_kernel<<<grid_for(D->count / 8), 256, 0, s>>>(reinterpret_cast<const uint16_t* const*>(D->tab),
-                                                           (int)D->n, D->shard, d_full);
+    dp_gather_kernel<<<kNumSMs * 4, 256, 0, s>>>(reinterpret_cast<const uint16_t* const*>(D->tab), (int)D->n,
+                                                (int)D->rank, D->shard, d_full);
     count_launch();
     MOE_TRY(dp_barrier(D, 3, s));
     MOE_CUDA_TRY(cudaGetLastError());
