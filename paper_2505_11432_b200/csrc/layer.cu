@@ -518,6 +518,10 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
             a.ldo = L->E;
             MOE_TRY(gemm_launch(L->p_router, a, s));
             MOE_TRY(launch_topk_from_logits(L->logits, Tr, L->E, k, L->ex_loc, L->gt_loc, s));
+        } else if (L->E <= 8 && h % 256 == 0) {
+            router_logits_mma_kernel<<<(unsigned)((Tr + 15) / 16), 256, 0, s>>>(
+                x_sym, L->wr, (int)Tr, (int)h, (int)L->E, L->logits, (int)k, L->ex_loc, L->gt_loc);
+            count_launch();
         } else if (wbytes <= 200 * 1024) {
             if (!L->router_attr) {
                 MOE_CUDA_TRY(cudaFuncSetAttribute(router_logits_smem_kernel,

@@ -10,6 +10,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "topk.cuh"
 
 namespace moe {
 
@@ -456,65 +457,98 @@ static __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot
 
 // K1 fast path: router weights staged in shared memory as fp32 (E*h*4 bytes),
 // one warp per FOUR tokens so every shared-memory weight load feeds four
-// FMAs (the kernel is bound by x's HBM stream, not by shared memory),
-// x streamed with 16-byte loads. E is processed in groups of 8.
+// FMAs; x streamed with 16-byte loads, RD vectors per token in flight per lane
+// (a rolling prefetch ring, 8 KB per warp) and the first ones issued before
+// the weights are staged, so the kernel runs at the x stream's HBM rate.
+// E is processed in groups of 8.
 static __global__ void __launch_bounds__(256, 1) router_logits_smem_kernel(
     const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr, int T, int h, int E,
     float* __restrict__ logits) {
     extern __shared__ __align__(16) float s_wf[];  // [E][h] fp32
-    for (int i = threadIdx.x; i < E * h / 8; i += blockDim.x) {
-        const uint4 v = reinterpret_cast<const uint4*>(wr)[i];
-        const float2 a = unpack_bf16x2(v.x), b = unpack_bf16x2(v.y), c = unpack_bf16x2(v.z), d = unpack_bf16x2(v.w);
-        reinterpret_cast<float4*>(s_wf)[2 * i] = make_float4(a.x, a.y, b.x, b.y);
-        reinterpret_cast<float4*>(s_wf)[2 * i + 1] = make_float4(c.x, c.y, d.x, d.y);
-    }
-    __syncthreads();
+    constexpr int RD = 4;                           // prefetch depth (iterations of 32 vectors)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const int nvec = h / 8;
-    for (int t0 = (blockIdx.x * wpb + warp) * 4; t0 < T; t0 += gridDim.x * wpb * 4) {
+    auto ldx = [&](int t0, int nt, int i, int v) -> uint4 {
+        return (i < nt && v < nvec) ? __ldg(reinterpret_cast<const uint4*>(x + (int64_t)(t0 + i) * h) + v)
+                                    : make_uint4(0, 0, 0, 0);
+    };
+    int t0 = (blockIdx.x * wpb + warp) * 4;
+    uint4 xn[RD][4];
+    {   // the first task's first vectors fly while W_r is staged
+        const int nt = t0 < T ? min(4, T - t0) : 0;
+#pragma unroll
+        for (int d = 0; d < RD; ++d)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xn[d][i] = ldx(t0, nt, i, lane + 32 * d);
+    }
+    {   // W_r -> smem fp32 with 8 independent 16 B loads in flight per thread
+        const int nw = E * h / 8;
+        constexpr int WU = 8;
+        for (int i0 = threadIdx.x; i0 < nw; i0 += blockDim.x * WU) {
+            uint4 v[WU];
+#pragma unroll
+            for (int u = 0; u < WU; ++u)
+                if (i0 + u * (int)blockDim.x < nw) v[u] = __ldg(reinterpret_cast<const uint4*>(wr) + i0 + u * blockDim.x);
+#pragma unroll
+            for (int u = 0; u < WU; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < nw) {
+                    const float2 a = unpack_bf16x2(v[u].x), b = unpack_bf16x2(v[u].y),
+                                 c = unpack_bf16x2(v[u].z), d = unpack_bf16x2(v[u].w);
+                    reinterpret_cast<float4*>(s_wf)[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+                    reinterpret_cast<float4*>(s_wf)[2 * i + 1] = make_float4(c.x, c.y, d.x, d.y);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    bool primed = true;
+    for (; t0 < T; t0 += gridDim.x * wpb * 4) {
         const int nt = min(4, T - t0);
         for (int e0 = 0; e0 < E; e0 += 8) {
+            if (!primed) {
+#pragma unroll
+                for (int d = 0; d < RD; ++d)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xn[d][i] = ldx(t0, nt, i, lane + 32 * d);
+            }
+            primed = false;
             float acc[4][8];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int q = 0; q < 8; ++q) acc[i][q] = 0.0f;
-            // software-pipelined x stream: next 16-byte vectors in flight while
-            // the current ones are multiplied
-            uint4 xn[4];
+            for (int v0 = lane; v0 < nvec; v0 += 32 * RD) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                xn[i] = (i < nt && lane < nvec) ? __ldg(reinterpret_cast<const uint4*>(x + (int64_t)(t0 + i) * h) + lane)
-                                               : make_uint4(0, 0, 0, 0);
-            for (int v = lane; v < nvec; v += 32) {
-                float xf[4][8];
+                for (int d = 0; d < RD; ++d) {
+                    const int v = v0 + 32 * d;
+                    float xf[4][8];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint4 xv = xn[i];
-                    const float2 a = unpack_bf16x2(xv.x), b = unpack_bf16x2(xv.y),
-                                 c = unpack_bf16x2(xv.z), d = unpack_bf16x2(xv.w);
-                    xf[i][0] = a.x; xf[i][1] = a.y; xf[i][2] = b.x; xf[i][3] = b.y;
-                    xf[i][4] = c.x; xf[i][5] = c.y; xf[i][6] = d.x; xf[i][7] = d.y;
-                }
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 xv = xn[d][i];
+                        const float2 a = unpack_bf16x2(xv.x), b = unpack_bf16x2(xv.y),
+                                     c = unpack_bf16x2(xv.z), dd = unpack_bf16x2(xv.w);
+                        xf[i][0] = a.x; xf[i][1] = a.y; xf[i][2] = b.x; xf[i][3] = b.y;
+                        xf[i][4] = c.x; xf[i][5] = c.y; xf[i][6] = dd.x; xf[i][7] = dd.y;
+                        xn[d][i] = ldx(t0, nt, i, v + 32 * RD);   // refill the slot RD steps ahead
+                    }
+                    if (v < nvec) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    xn[i] = (i < nt && v + 32 < nvec)
-                                ? __ldg(reinterpret_cast<const uint4*>(x + (int64_t)(t0 + i) * h) + v + 32)
-                                : make_uint4(0, 0, 0, 0);
+                        for (int q = 0; q < 8; ++q) {
+                            if (e0 + q < E) {
+                                const float4 w0 = reinterpret_cast<const float4*>(s_wf + (int64_t)(e0 + q) * h)[2 * v];
+                                const float4 w1 = reinterpret_cast<const float4*>(s_wf + (int64_t)(e0 + q) * h)[2 * v + 1];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    if (e0 + q < E) {
-                        const float4 w0 = reinterpret_cast<const float4*>(s_wf + (int64_t)(e0 + q) * h)[2 * v];
-                        const float4 w1 = reinterpret_cast<const float4*>(s_wf + (int64_t)(e0 + q) * h)[2 * v + 1];
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            float s = acc[i][q];
-                            s = fmaf(xf[i][0], w0.x, s); s = fmaf(xf[i][1], w0.y, s);
-                            s = fmaf(xf[i][2], w0.z, s); s = fmaf(xf[i][3], w0.w, s);
-                            s = fmaf(xf[i][4], w1.x, s); s = fmaf(xf[i][5], w1.y, s);
-                            s = fmaf(xf[i][6], w1.z, s); s = fmaf(xf[i][7], w1.w, s);
-                            acc[i][q] = s;
+                                for (int i = 0; i < 4; ++i) {
+                                    float s = acc[i][q];
+                                    s = fmaf(xf[i][0], w0.x, s); s = fmaf(xf[i][1], w0.y, s);
+                                    s = fmaf(xf[i][2], w0.z, s); s = fmaf(xf[i][3], w0.w, s);
+                                    s = fmaf(xf[i][4], w1.x, s); s = fmaf(xf[i][5], w1.y, s);
+                                    s = fmaf(xf[i][6], w1.z, s); s = fmaf(xf[i][7], w1.w, s);
+                                    acc[i][q] = s;
+                                }
+                            }
                         }
                     }
                 }
@@ -529,6 +563,88 @@ static __global__ void __launch_bounds__(256, 1) router_logits_smem_kernel(
                     if (lane == 0 && i < nt && e0 + q < E) logits[(int64_t)(t0 + i) * E + e0 + q] = a;
                 }
         }
+    }
+}
+
+// K1 for E <= 8 (Mixtral shape): logits[T, E] = x . W_r^T with warp-level
+// bf16 tensor-core MMAs (m16n8k16, fp32 accumulate; n = 8 = E). A CTA owns 16
+// tokens; its 8 warps split h into 8 slices and the slices' partial logits
+// are summed in fixed warp order through shared memory (deterministic). The
+// contraction index inside every 32-column window is permuted identically for
+// x and W_r (lane c's fragment slots {2c, 2c+1, 2c+8, 2c+9} of step t are the
+// physical columns 8c + 4t + {0..3}), so each lane feeds two MMAs from one
+// 16-byte load per token row: the kernel is a pure stream of x.
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+static __global__ void __launch_bounds__(256) router_logits_mma_kernel(
+    const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr, int T, int h, int E,
+    float* __restrict__ logits, int k, int32_t* __restrict__ experts, float* __restrict__ gates) {
+    __shared__ float red[8][16][8];
+    __shared__ float s_lg[16][8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, c = lane & 3;
+    const int t0 = blockIdx.x * 16;
+    const int slice = h / 8, k_lo = warp * slice;
+    const bool r0 = t0 + g < T, r1 = t0 + g + 8 < T, ev = g < E;
+    const uint4* xa = reinterpret_cast<const uint4*>(x + (int64_t)(t0 + g) * h + k_lo) + c;
+    const uint4* xb = reinterpret_cast<const uint4*>(x + (int64_t)(t0 + g + 8) * h + k_lo) + c;
+    const uint4* wb = reinterpret_cast<const uint4*>(wr + (int64_t)g * h + k_lo) + c;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    constexpr int WB = 4;   // 32-column windows per batch; two batches in flight (24 x 16 B per lane)
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    const int nwin = slice / 32;
+    auto load = [&](uint4 (&va)[WB], uint4 (&vb)[WB], uint4 (&vw)[WB], int w0) {
+#pragma unroll
+        for (int u = 0; u < WB; ++u) {
+            const bool in = w0 + u < nwin;
+            va[u] = (in && r0) ? __ldg(xa + (w0 + u) * 4) : z;
+            vb[u] = (in && r1) ? __ldg(xb + (w0 + u) * 4) : z;
+            vw[u] = (in && ev) ? __ldg(wb + (w0 + u) * 4) : z;
+        }
+    };
+    auto mma = [&](const uint4 (&va)[WB], const uint4 (&vb)[WB], const uint4 (&vw)[WB]) {
+#pragma unroll
+        for (int u = 0; u < WB; ++u) {
+            mma_bf16_16816(acc, va[u].x, vb[u].x, va[u].y, vb[u].y, vw[u].x, vw[u].y);
+            mma_bf16_16816(acc, va[u].z, vb[u].z, va[u].w, vb[u].w, vw[u].z, vw[u].w);
+        }
+    };
+    uint4 a0[WB], b0[WB], w0v[WB], a1[WB], b1[WB], w1v[WB];
+    load(a0, b0, w0v, 0);
+    for (int w0 = 0; w0 < nwin; w0 += 2 * WB) {
+        load(a1, b1, w1v, w0 + WB);         // next batch in flight during this one's MMAs
+        mma(a0, b0, w0v);
+        if (w0 + 2 * WB < nwin) load(a0, b0, w0v, w0 + 2 * WB);
+        if (w0 + WB < nwin) mma(a1, b1, w1v);
+    }
+    red[warp][g][2 * c] = acc[0];
+    red[warp][g][2 * c + 1] = acc[1];
+    red[warp][g + 8][2 * c] = acc[2];
+    red[warp][g + 8][2 * c + 1] = acc[3];
+    __syncthreads();
+    if (threadIdx.x < 128) {
+        const int r = threadIdx.x >> 3, e = threadIdx.x & 7;
+        float sum = red[0][r][e];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) sum += red[w][r][e];
+        s_lg[r][e] = sum;
+        if (e < E && t0 + r < T) logits[(int64_t)(t0 + r) * E + e] = sum;
+    }
+    __syncthreads();
+    // top-k + softmax of the CTA's 16 tokens, two per warp (the separate
+    // topk_from_logits launch folded in)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int r = 2 * warp + q;
+        if (t0 + r < T)
+            topk_select(s_lg[r], E, k, experts + (int64_t)(t0 + r) * k, gates + (int64_t)(t0 + r) * k, lane);
     }
 }
 

@@ -9,6 +9,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "topk.cuh"
 #include "runtime.h"
 
 namespace moe {
@@ -20,53 +21,6 @@ namespace moe {
 // of up to 32 experts over its slice of h (16-byte vectors), then a warp
 // butterfly reduction. Wr rows are read through L1/L2 (E*h*2 bytes, reused
 // by every token of the block).
-__device__ __forceinline__ void topk_select(const float* lg, int E, int k, int32_t* ex,
-                                            float* gt, int lane) {
-    // warp-parallel argmax rounds, ties -> lower expert id
-    unsigned long long taken_lo = 0;  // bitset for lanes' candidates (E <= 32*? handled by loop)
-    (void)taken_lo;
-    float sel_val[8];
-    int sel_id[8];
-    for (int j = 0; j < k; ++j) {
-        float best = -INFINITY;
-        int bid = 0x7fffffff;
-        for (int e = lane; e < E; e += 32) {
-            bool taken = false;
-            for (int i = 0; i < j; ++i) taken |= (sel_id[i] == e);
-            const float v = lg[e];
-            if (!taken && (v > best || (v == best && e < bid) || bid == 0x7fffffff)) {
-                best = v;
-                bid = e;
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, best, off);
-            const int oid = __shfl_xor_sync(0xffffffffu, bid, off);
-            if (oid != 0x7fffffff && (bid == 0x7fffffff || ov > best || (ov == best && oid < bid))) {
-                best = ov;
-                bid = oid;
-            }
-        }
-        sel_val[j] = best;
-        sel_id[j] = bid;
-    }
-    if (lane == 0) {
-        // gates = softmax over the k selected logits (max-subtracted, fp32)
-        const float m = sel_val[0];
-        float s = 0.0f;
-        float ev[8];
-        for (int j = 0; j < k; ++j) {
-            ev[j] = expf(sel_val[j] - m);
-            s += ev[j];
-        }
-        for (int j = 0; j < k; ++j) {
-            ex[j] = sel_id[j];
-            gt[j] = ev[j] / s;
-        }
-    }
-}
-
 __global__ void router_topk_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr,
                                    int T, int h, int E, int k, float* __restrict__ logits,
                                    int32_t* __restrict__ experts, float* __restrict__ gates) {
