@@ -122,7 +122,7 @@ struct TileInfo {
 
 template <int TILE_M, bool K_GROUPED>
 __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const int* row_off,
-                                                const GemmArgs& a, int G, int n_tiles) {
+                                                const int* kb, const GemmArgs& a, int G, int n_tiles) {
     int lo = 0, hi = G - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
@@ -134,7 +134,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
     int li = t - prefix[lo];
     ti.half_tile = 0;
     if (!K_GROUPED) {
-        const int rows = a.group_rows[lo];
+        const int rows = row_off[lo + 1] - row_off[lo];
         const int mt = (rows + TILE_M - 1) / TILE_M;
         const int mc = (a.m_chunk > 0 && a.m_chunk < mt) ? a.m_chunk : mt;
         const int full = mc * n_tiles;
@@ -151,7 +151,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
         // of B's (small) contraction panel from L2
         ti.n = li % n_tiles;
         ti.m = li / n_tiles;
-        ti.kblocks = a.group_k_rows ? (a.group_k_rows[lo] + 63) >> 6 : a.group_rows[lo] >> 6;
+        ti.kblocks = kb[lo];
         ti.row0 = row_off[lo];   // contraction row offset
     }
     return ti;
@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
     __shared__ int prefix[Cfg::MAX_GROUPS + 1];    // tile prefix per group
     __shared__ int s_rowoff[Cfg::MAX_GROUPS + 1];  // padded row offset per group
+    __shared__ int s_kb[Cfg::MAX_GROUPS];          // K-grouped: k blocks per group
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -625,18 +626,46 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
     // --- setup ---------------------------------------------------------------
-    if (threadIdx.x == 0) {
-        int acc = 0, racc = 0;
-        for (int g = 0; g < G; ++g) {
-            prefix[g] = acc;
-            s_rowoff[g] = racc;
-            const int rows = args.group_rows[g];
-            racc += rows;
-            if (!K_GROUPED) acc += ((rows + TILE_M - 1) / TILE_M) * n_tiles;
-            else acc += (args.K / TILE_M) * n_tiles;
+    // group tables in shared memory, built by warp 0: every group's row count is
+    // loaded in one round trip (lane + 32 j), then a shuffle scan per 32 groups.
+    // The roles' per-tile decode reads only shared memory (no global loads on
+    // the tile path).
+    if (warp == 0) {
+        constexpr int NJ = Cfg::MAX_GROUPS / 32;
+        int rws[NJ], kr[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int g = lane + 32 * j;
+            rws[j] = g < G ? args.group_rows[g] : 0;
+            kr[j] = (K_GROUPED && args.group_k_rows && g < G) ? args.group_k_rows[g] : rws[j];
         }
-        prefix[G] = acc;
-        s_rowoff[G] = racc;
+        int carry_t = 0, carry_r = 0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int g = lane + 32 * j;
+            const int rows = rws[j];
+            const int tiles = g < G ? (K_GROUPED ? (args.K / TILE_M) * n_tiles
+                                                 : ((rows + TILE_M - 1) / TILE_M) * n_tiles)
+                                    : 0;
+            int it = tiles, ir = rows;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int ut = __shfl_up_sync(0xffffffffu, it, off);
+                const int ur = __shfl_up_sync(0xffffffffu, ir, off);
+                if (lane >= off) { it += ut; ir += ur; }
+            }
+            if (g < G) {
+                prefix[g] = carry_t + it - tiles;
+                s_rowoff[g] = carry_r + ir - rows;
+                if (K_GROUPED) s_kb[g] = (kr[j] + 63) >> 6;
+            }
+            carry_t += __shfl_sync(0xffffffffu, it, 31);
+            carry_r += __shfl_sync(0xffffffffu, ir, 31);
+        }
+        if (lane == 0) {
+            prefix[G] = carry_t;
+            s_rowoff[G] = carry_r;
+        }
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
@@ -670,7 +699,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             const int arow = (int)cta_rank * BM;       // this CTA's A rows within the tile
             const int bcol = (int)cta_rank * BN_CTA;   // this CTA's B rows/cols within the tile
             for (int t = unit; t < total_tiles; t += nunits) {
-                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, s_kb, args, G, n_tiles);
                 for (int kb = 0; kb < ti.kblocks; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
@@ -740,7 +769,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int t = unit; t < total_tiles; t += nunits) {
-                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+                const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, s_kb, args, G, n_tiles);
                 if (ti.kblocks == 0) continue;
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -784,7 +813,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = unit; t < total_tiles; t += nunits) {
-            const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, args, G, n_tiles);
+            const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, s_kb, args, G, n_tiles);
             const int n0 = ti.n * BN;
             int64_t orow;
             if (K_GROUPED) {

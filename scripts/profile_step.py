@@ -11,6 +11,9 @@ from paper_2505_11432_b200.layer import MoELayer
 cfg = dict(h=4096, f=14336, E=8, k=2, Tr=4096)
 if len(sys.argv) > 1 and sys.argv[1] == "deepseek":
     cfg = dict(h=7168, f=2048, E=256, k=8, Tr=4096)
+if len(sys.argv) > 1 and sys.argv[1] == "deepseek_ep4":
+    # one rank's expert work at EP = 4 (64 local experts, ~512 rows each) on one GPU
+    cfg = dict(h=7168, f=2048, E=64, k=8, Tr=4096)
 h, f, E, k, Tr = cfg["h"], cfg["f"], cfg["E"], cfg["k"], cfg["Tr"]
 g = torch.Generator(device="cuda").manual_seed(42)
 w1 = (torch.randn(E, 2 * f, h, device="cuda", generator=g) / h ** 0.5).bfloat16()
