@@ -32,7 +32,8 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2505_11432_b200.layer import MoELayer
 
-    Tr, h, f, E, k = int(os.environ.get("MP_TR", 256)), 512, 512, 8, 2
+    Tr, h, f = int(os.environ.get("MP_TR", 256)), 512, 512
+    E, k = int(os.environ.get("MP_E", 8)), int(os.environ.get("MP_K", 2))
     cf = float(os.environ.get("MP_CF", "0"))
     T = Tr * n
     el = E // n
