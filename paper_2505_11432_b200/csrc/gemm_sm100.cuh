@@ -19,8 +19,8 @@
 //   read both CTAs' shared memory, halving the per-SM operand traffic.
 //
 // Roles (320 threads, 1 CTA per SM, persistent over a static tile stride):
-//   warp 0 lane 0 : TMA producer (multi-stage smem ring, 128B swizzle)
-//   warp 1        : TMEM allocator; lane 0 of the leader CTA issues tcgen05.mma
+//   warp 0        : TMA producer (multi-stage smem ring, 128B swizzle; one elected lane issues)
+//   warp 1        : TMEM allocator; in the leader CTA one elected lane issues tcgen05.mma
 //   warps 2..9    : epilogue, two warps per TMEM lane quarter (each half of the
 //                   columns); TMEM double-buffered so tile i's epilogue
 //                   overlaps tile i+1's MMA.
@@ -187,6 +187,71 @@ __device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, u
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// TMA / expect-tx issued by one elected lane of a convergent warp
+__device__ __forceinline__ void tma_load_2d_2sm_warp(void* smem_dst, const CUtensorMap* map,
+                                                     uint32_t leader_bar, int32_t c0, int32_t c1) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_warp(void* smem_dst, const CUtensorMap* map,
+                                                 uint64_t* bar, int32_t c0, int32_t c1) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_warp(uint64_t* bar, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)), "r"(bytes)
+        : "memory");
+}
+
+// Warp-convergent issue: the whole warp executes the asm and elect.sync picks
+// the one lane that issues, so the operands stay in (uniform) registers with
+// no per-instruction broadcast loop around the MMA.
+__device__ __forceinline__ void umma_bf16_2sm_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                   uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_bf16_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_2sm_mc_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\t.reg .pred e;\n\tmov.b16 m, 3;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}"
+        ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+        ::"r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
@@ -693,7 +758,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
 
     if (warp == 0) {
         // ===================== TMA producer =====================
-        if (lane == 0) {
+        // whole warp in convergence, one elected lane issues (as for the MMA)
+        {
             int stage = 0;
             uint32_t phase = 0;
             const int arow = (int)cta_rank * BM;       // this CTA's A rows within the tile
@@ -708,13 +774,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                     uint32_t fb_leader = 0;
                     if (CG == 2) {
                         fb_leader = map_to_cta(fb, 0);
-                        if (leader) mbar_arrive_expect_tx(fb, CG * Cfg::STAGE_BYTES);
+                        if (leader) mbar_arrive_expect_tx_warp(fb, CG * Cfg::STAGE_BYTES);
                     } else {
-                        mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES);
+                        mbar_arrive_expect_tx_warp(fb, Cfg::STAGE_BYTES);
                     }
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
-                        if (CG == 2) tma_load_2d_2sm(dst, map, fb_leader, c0, c1);
-                        else tma_load_2d(dst, map, fb, c0, c1);
+                        if (CG == 2) tma_load_2d_2sm_warp(dst, map, fb_leader, c0, c1);
+                        else tma_load_2d_warp(dst, map, fb, c0, c1);
                     };
                     if (!K_GROUPED) {
                         if (DISPATCH && kb == 0) {
@@ -722,15 +788,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                             // 128-row block) have landed
                             const uint32_t* rdy = &args.ready[ti.row0 / BM];
                             const int nblk = ti.half_tile ? 1 : CG;
-                            const uint64_t t0 = globaltimer();
-                            for (int b = 0; b < nblk; ++b)
-                                while (ld_acquire_gpu(rdy + b) < (uint32_t)BM) {
-                                    if (globaltimer() - t0 > 4000000000ull) {
-                                        atomicExch(args.err, 2);
-                                        break;
+                            if (lane == 0) {
+                                const uint64_t t0 = globaltimer();
+                                for (int b = 0; b < nblk; ++b)
+                                    while (ld_acquire_gpu(rdy + b) < (uint32_t)BM) {
+                                        if (globaltimer() - t0 > 4000000000ull) {
+                                            atomicExch(args.err, 2);
+                                            break;
+                                        }
                                     }
-                                }
-                            fence_proxy_async_global();
+                            }
+                            __syncwarp();
+                            fence_proxy_async_global();   // every lane: the issuing lane is elected
                         }
                         // half tile: each CTA of the pair takes 64 rows (the box's other
                         // 64 rows are loaded but not read by the M = 128 UMMA)
@@ -761,9 +830,21 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
-        if (lane == 0 && leader) {
+        // The whole warp walks the tile / k-block sequence in convergence, so
+        // descriptors and TMEM addresses stay warp-uniform (uniform registers)
+        // and one elected lane issues: no per-MMA register broadcast loops.
+        if (leader) {
             constexpr uint32_t idesc_full = make_idesc(TILE_M, BN, 1, A_MN, B_MN);
             constexpr uint32_t idesc_half = make_idesc(128, BN, 1, A_MN, B_MN);
+            // stage s's descriptors = stage 0's + s * STAGE_BYTES / 16 (14-bit
+            // address field, smem < 256 KB); k step within a stage: +32 B
+            // (K-major) or +2048 B (MN-major), i.e. +2 / +128 in 16-byte units
+            const uint32_t s0 = smem_u32(smem);
+            const uint64_t a_base = A_MN ? make_sdesc(s0, 8192, 1024) : make_sdesc(s0, 16, 1024);
+            const uint64_t b_base = B_MN ? make_sdesc(s0 + Cfg::A_BYTES, 8192, 1024)
+                                         : make_sdesc(s0 + Cfg::A_BYTES, 16, 1024);
+            constexpr uint64_t a_kstep = A_MN ? 128 : 2, b_kstep = B_MN ? 128 : 2;
+            constexpr uint64_t stage_step = Cfg::STAGE_BYTES >> 4;
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -778,23 +859,20 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                 for (int kb = 0; kb < ti.kblocks; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-                    const uint32_t sb = sa + Cfg::A_BYTES;
+                    const uint64_t ad0 = a_base + (uint64_t)stage * stage_step;
+                    const uint64_t bd0 = b_base + (uint64_t)stage * stage_step;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        const uint64_t ad = A_MN ? make_sdesc(sa + kk * 2048, 8192, 1024)
-                                                 : make_sdesc(sa + kk * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? make_sdesc(sb + kk * 2048, 8192, 1024)
-                                                 : make_sdesc(sb + kk * 32, 16, 1024);
-                        if (CG == 2) umma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-                        else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        const uint64_t ad = ad0 + kk * a_kstep, bd = bd0 + kk * b_kstep;
+                        if (CG == 2) umma_bf16_2sm_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        else umma_bf16_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                     }
-                    if (CG == 2) umma_commit_2sm_mc(&empty_bar[stage]);
-                    else umma_commit(&empty_bar[stage]);
+                    if (CG == 2) umma_commit_2sm_mc_warp(&empty_bar[stage]);
+                    else umma_commit_warp(&empty_bar[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if (CG == 2) umma_commit_2sm_mc(&tfull_bar[acc]);
-                else umma_commit(&tfull_bar[acc]);
+                if (CG == 2) umma_commit_2sm_mc_warp(&tfull_bar[acc]);
+                else umma_commit_warp(&tfull_bar[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }

@@ -4,7 +4,7 @@ epilogue), eager phase timing."""
 import os
 import sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.getcwd())
 from paper_2505_11432_b200 import ops
 from paper_2505_11432_b200.layer import MoELayer
 
