@@ -401,6 +401,15 @@ def run_ours(args, cfg):
         rb = Tr * h * 2 + E * h * 2              # router: x + W_r
         sb = 2 * rows_pad * h * 2                # scatter: read rows + write permuted rows
         cb = (k + 1) * Tr * h * 2                # combine: k staged rows in + y out
+        if world > 1 and "dispatch" in pu and pu["dispatch"] > 0:
+            # NVLink pull rate of the standalone dispatch kernel (rows whose token
+            # lives on a peer), against 900 GB/s per direction
+            osr_u = L.routing()["out_source_rank"]
+            rrows = int((osr_u != rank).sum().item())
+            pull = rrows * h * 2 / (pu["dispatch"] * 1e6)
+            nvlink_pull = {"remote_rows": rrows, "ms": pu["dispatch"], "GBps": pull, "frac_900": pull / 900.0}
+        else:
+            nvlink_pull = None
         membw = {kk: {"ms": pu[ph], "GBps": b / (pu[ph] * 1e6), "frac_hbm": b / (pu[ph] * 1e6) / hbm}
                  for kk, ph, b in (("router", "route", rb), ("scatter", "dispatch", sb), ("combine", "combine", cb))
                  if ph in pu and pu[ph] > 0}
@@ -524,9 +533,14 @@ def run_ours(args, cfg):
                     "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                     "frac": achieved / peaks["bf16_sus"], "traffic": traffic,
                     "algorithmic_bytes": fc1_bytes, "peak_kind": f"bf16 sustained ({peaks['src']})"}
-        roof.update({"step_bound": "hbm" if st_hbm > st_tc else "tensor",
-                     "step_roofline_ms": 1000 * max(st_tc, st_hbm),
-                     "step_frac": 1000 * max(st_tc, st_hbm) / ms,
+        # n > 1: NVLink bytes of this rank's fused exchanges at the measured link rate
+        st_link = (nvlink["bytes_per_step"] / 770e9) if nvlink else 0.0
+        bounds = {"tensor": st_tc, "hbm": st_hbm, "nvlink": st_link}
+        sb_name = max(bounds, key=bounds.get)
+        roof.update({"step_bound": sb_name,
+                     "step_roofline_ms": 1000 * bounds[sb_name],
+                     "step_frac": 1000 * bounds[sb_name] / ms,
+                     "step_bound_ms": {kk: round(1000 * v, 4) for kk, v in bounds.items()},
                      "step_tflops": total_flops / (ms / 1000.0) / 1e12})
         line = {
             "metric": "moe_layer_fwd_bwd_tokens_per_s", "value": value, "unit": "tokens/s",
@@ -545,6 +559,7 @@ def run_ours(args, cfg):
             "memory_bound_ops": membw,
             "exposed_comm": exposed,
             "nvlink": nvlink,
+            "nvlink_dispatch_pull": nvlink_pull if membw is not None else None,
             "nccl_a2a_cublas_baseline": None if nccl_ms is None else {
                 "ms_per_step": nccl_ms, "tokens_per_s": n * Tr / (nccl_ms / 1000.0),
                 "speedup_of_fused": nccl_ms / ms,

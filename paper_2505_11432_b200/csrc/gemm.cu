@@ -1,11 +1,29 @@
 // gemm.cu — host launchers for the tcgen05 grouped GEMM (gemm_sm100.cuh)
 // and the C-ABI `moe_grouped_gemm` operator (reference OpKind::grouped_gemm,
 // simsched.hpp:32-44).
+#include <atomic>
 #include <cstdlib>
+#include <mutex>
 
 #include "gemm.h"
 
 namespace moe {
+
+// Dynamic tile schedule counters: one int per launch from a per-device ring,
+// zeroed on the launch's stream just before it (graph-capturable). A slot is
+// reused only after kCounters later launches.
+static int* tile_counter_slot(int dev) {
+    constexpr int kDevices = 64, kCounters = 4096;
+    static int* base[kDevices] = {};
+    static std::atomic<unsigned> next[kDevices];
+    static std::mutex mu;
+    if (dev < 0 || dev >= kDevices) return nullptr;
+    if (!base[dev]) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!base[dev] && cudaMalloc(&base[dev], kCounters * sizeof(int)) != cudaSuccess) return nullptr;
+    }
+    return base[dev] + (next[dev].fetch_add(1) % kCounters);
+}
 
 template <int BN, int CG, bool A_MN, bool B_MN, bool KG, int EPI, bool DISP = false>
 static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
@@ -43,9 +61,17 @@ static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, cons
     return MOE_OK;
 }
 
-moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s) {
-    MOE_CHECK_ARG(a.G >= 1 && a.G <= 256, "grouped GEMM: 1 <= groups <= 256");
+moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) {
+    MOE_CHECK_ARG(args.G >= 1 && args.G <= 256, "grouped GEMM: 1 <= groups <= 256");
     const int grid = p.grid > 0 ? p.grid : kNumSMs;
+    GemmArgs a = args;
+    static const bool static_tiles = getenv("MOE_STATIC_TILES") != nullptr;
+    if (!a.tile_counter && !static_tiles && !p.k_grouped) {
+        int dev = 0;
+        MOE_CUDA_TRY(cudaGetDevice(&dev));
+        a.tile_counter = tile_counter_slot(dev);
+        if (a.tile_counter) MOE_CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), s));
+    }
 #define MOE_GEMM_CASE(BN, CG, AMN, BMN, KG, EPI)                                              \
     if (p.bn == BN && p.cg == CG && p.a_mn == AMN && p.b_mn == BMN && p.k_grouped == KG &&   \
         p.epi == EPI && !p.dispatch)                                                          \

@@ -92,6 +92,10 @@ struct GemmArgs {
     // already-landed row dup_src[pp] (< pp) locally instead of pulling it again
     const int32_t* dup_src;     // [padded rows] earlier row of the same token, -1 = pull
     uint32_t* row_done;         // [padded rows] set once a row has landed
+    // dynamic tile schedule: zeroed before the launch; the leader CTA's producer
+    // takes tiles in order with an atomic and hands them to every role through a
+    // shared-memory queue (nullptr = static stride schedule)
+    int* tile_counter;
 };
 
 template <int BN, int CG>
@@ -189,6 +193,25 @@ __device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, u
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// ---- dynamic tile queue helpers (cluster scope) ----------------------------
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void st_shared_cluster(uint32_t cluster_addr, int v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+
 // TMA / expect-tx issued by one elected lane of a convergent warp
 __device__ __forceinline__ void tma_load_2d_2sm_warp(void* smem_dst, const CUtensorMap* map,
                                                      uint32_t leader_bar, int32_t c0, int32_t c1) {
@@ -680,6 +703,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     __shared__ int prefix[Cfg::MAX_GROUPS + 1];    // tile prefix per group
     __shared__ int s_rowoff[Cfg::MAX_GROUPS + 1];  // padded row offset per group
     __shared__ int s_kb[Cfg::MAX_GROUPS];          // K-grouped: k blocks per group
+    constexpr int QD = 8;                           // tile queue depth
+    __shared__ int s_tq[QD];
+    __shared__ __align__(8) uint64_t s_tq_full[QD], s_tq_empty[QD];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -743,6 +769,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             mbar_init(&tfull_bar[a], 1);
             mbar_init(&tempty_bar[a], Cfg::EPI_WARPS * CG);
         }
+        // queue consumers: MMA + epilogue warps of the leader, producer +
+        // epilogue warps of the peer
+        for (int q = 0; q < QD; ++q) {
+            mbar_init(&s_tq_full[q], 1);
+            mbar_init(&s_tq_empty[q], (1 + Cfg::EPI_WARPS) * CG);
+        }
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -755,6 +787,61 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int total_tiles = prefix[G];
+    // dynamic for M-grouped GEMMs (M = 128 tail tiles and dispatch waits make
+    // tile costs uneven, and a drifting static stride breaks the L2 sharing of
+    // weight panels: 2.3x DRAM reads measured); the K-grouped wgrads keep the
+    // static stride, which measured faster for them
+    const bool dyn = !K_GROUPED && args.tile_counter != nullptr;
+    // i-th tile of this CTA (pair): static stride, or dynamic. The leader's
+    // producer fetches (atomic, in order) and publishes to the local queue and,
+    // for a pair, to the peer's; every other role dequeues. -1 ends the loop.
+    // The producer publishes tiles LA ahead of the one it is loading, so the
+    // peer CTA's producer and the consumers see a tile well before its loads
+    // start (cross-CTA signalling stays off the critical path of short tiles),
+    // and the next atomic is always in flight.
+    constexpr int LA = 3;   // < QD: the producer's own slot is never overwritten
+    int t_ahead = (dyn && warp == 0 && lane == 0 && leader) ? atomicAdd(args.tile_counter, 1) : 0;
+    int published = 0;
+    bool ended = false;
+    auto fetch_tile = [&](int i) -> int {
+        if (!dyn) return unit + i * nunits < total_tiles ? unit + i * nunits : -1;
+        while (!ended && published <= i + LA) {
+            const int slot = published % QD;
+            const uint32_t ph = (uint32_t)(published / QD) & 1u;
+            int t = 0;
+            if (lane == 0) {
+                t = t_ahead;
+                if (t >= total_tiles) t = -1;
+                else t_ahead = atomicAdd(args.tile_counter, 1);
+                mbar_wait(&s_tq_empty[slot], ph ^ 1u);
+                s_tq[slot] = t;
+                if (CG == 2) {
+                    st_shared_cluster(map_to_cta(&s_tq[slot], 1), t);
+                    mbar_arrive_release_cluster(map_to_cta(&s_tq_full[slot], 1));
+                }
+                mbar_arrive(&s_tq_full[slot]);
+            }
+            t = __shfl_sync(0xffffffffu, t, 0);
+            ended = t < 0;
+            ++published;
+        }
+        // this CTA wrote slot i itself (published > i)
+        return *reinterpret_cast<volatile int*>(&s_tq[i % QD]);
+    };
+    auto next_tile = [&](int i) -> int {
+        if (!dyn) return unit + i * nunits < total_tiles ? unit + i * nunits : -1;
+        const int slot = i % QD;
+        const uint32_t ph = (uint32_t)(i / QD) & 1u;
+        int t = 0;
+        if (lane == 0) {
+            while (!mbar_try_wait_cluster(&s_tq_full[slot], ph)) {
+            }
+            t = *reinterpret_cast<volatile int*>(&s_tq[slot]);
+            if (CG == 2 && !leader) mbar_arrive_release_cluster(map_to_cta(&s_tq_empty[slot], 0));
+            else mbar_arrive(&s_tq_empty[slot]);
+        }
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -764,7 +851,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             uint32_t phase = 0;
             const int arow = (int)cta_rank * BM;       // this CTA's A rows within the tile
             const int bcol = (int)cta_rank * BN_CTA;   // this CTA's B rows/cols within the tile
-            for (int t = unit; t < total_tiles; t += nunits) {
+            for (int it = 0;; ++it) {
+                const int t = leader ? fetch_tile(it) : next_tile(it);
+                if (t < 0) break;
                 const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, s_kb, args, G, n_tiles);
                 for (int kb = 0; kb < ti.kblocks; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -849,7 +938,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = unit; t < total_tiles; t += nunits) {
+            for (int it = 0;; ++it) {
+                const int t = next_tile(it);
+                if (t < 0) break;
                 const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, s_kb, args, G, n_tiles);
                 if (ti.kblocks == 0) continue;
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -890,7 +981,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
         const uint32_t tempty_leader = CG == 2 ? map_to_cta(&tempty_bar[0], 0) : 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = unit; t < total_tiles; t += nunits) {
+        for (int it = 0;; ++it) {
+            const int t = next_tile(it);
+            if (t < 0) break;
             const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, s_kb, args, G, n_tiles);
             const int n0 = ti.n * BN;
             int64_t orow;

@@ -2,7 +2,7 @@
 import os
 import sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.getcwd())
 from paper_2505_11432_b200 import ops
 
 def timeit(fn, reps=10):
