@@ -65,7 +65,7 @@ static __global__ void dup_src_kernel(const int32_t* __restrict__ pad_row_tok, c
 // Dispatch: dst[pp, :] = src_rank_buffer[t_local, :] for real rows, 0 for
 // pads (AG + local scatter fused: rows are pulled straight from the owning
 // rank's buffer over NVLink into permuted order).
-// One warp per row, 16-byte vectors, 4 in flight per lane.
+// One warp per row, 16-byte vectors, 16 in flight per lane.
 static __global__ void dispatch_rows_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad,
                                      int k, int tokens_per_rank, int h,
                                      const uint16_t* const* __restrict__ src_bufs,
@@ -86,12 +86,17 @@ static __global__ void dispatch_rows_kernel(const int32_t* __restrict__ pad_row_
         const int t = i / k;
         const int src = t / tokens_per_rank;
         const uint4* s = reinterpret_cast<const uint4*>(src_bufs[src] + (int64_t)(t - src * tokens_per_rank) * h);
-        int v = lane;
-        for (; v + 96 < nvec; v += 128) {
-            const uint4 a0 = s[v], a1 = s[v + 32], a2 = s[v + 64], a3 = s[v + 96];
-            d[v] = a0; d[v + 32] = a1; d[v + 64] = a2; d[v + 96] = a3;
+        // 16 x 16 B loads in flight per lane (a whole 4096-wide row), predicated tail
+        constexpr int U = 16;
+        for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+            uint4 r[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (v0 + 32 * q < nvec) r[q] = s[v0 + 32 * q];
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (v0 + 32 * q < nvec) d[v0 + 32 * q] = r[q];
         }
-        for (; v < nvec; v += 32) d[v] = s[v];
     }
 }
 
