@@ -795,11 +795,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     // i-th tile of this CTA (pair): static stride, or dynamic. The leader's
     // producer fetches (atomic, in order) and publishes to the local queue and,
     // for a pair, to the peer's; every other role dequeues. -1 ends the loop.
-    // The producer publishes tiles LA ahead of the one it is loading, so the
-    // peer CTA's producer and the consumers see a tile well before its loads
-    // start (cross-CTA signalling stays off the critical path of short tiles),
-    // and the next atomic is always in flight.
-    constexpr int LA = 3;   // < QD: the producer's own slot is never overwritten
+    // The producer claims a tile only when it starts loading it (LA = 0): the
+    // tiles in flight across the grid then form one contiguous window of the
+    // tile order, so concurrent tiles share their weight / activation panels in
+    // L2. (Claiming ahead spreads each CTA's next claims over several waves and
+    // doubled the DRAM reads of the Mixtral fc1-dgrad.) The next atomic is
+    // always in flight; the peer CTA learns the tile while the MMA still works
+    // through the 6 staged k-blocks of the previous one.
+    constexpr int LA = 0;   // < QD: the producer's own slot is never overwritten
     int t_ahead = (dyn && warp == 0 && lane == 0 && leader) ? atomicAdd(args.tile_counter, 1) : 0;
     int published = 0;
     bool ended = false;
