@@ -484,7 +484,7 @@ def run_ours(args, cfg):
         # (layer.cu `dedup`; the gate-after backward pulls every row)
         tok = rt["row_map_in"].cpu()[remote] // L.k
         remote_tokens = int(torch.unique(tok).numel())
-        dedup = os.environ.get("MOE_DISPATCH_DEDUP") is not None and L.k > 1 and L.E // n > 1
+        dedup = os.environ.get("MOE_NO_DISPATCH_DEDUP") is None and L.k > 1 and L.E // n > 1
         pulled_fwd = remote_tokens if dedup else remote_rows
         pulled_bwd = remote_rows if cfg.get("gate") == "after_fc2_out" else pulled_fwd
         bpe = 1 if cfg.get("comm", "bf16") == "fp8" else 2

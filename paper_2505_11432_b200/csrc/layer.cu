@@ -402,10 +402,9 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     // the unfused (reference-structure) dispatch path is kept for A/B runs;
     // gate-after-fc2 backward needs the fused path's row scaling
     L->fused_dispatch = getenv("MOE_UNFUSED_DISPATCH") == nullptr || L->gate_after || L->fp8;
-    // off by default: at EP = 4 the pulls are hidden under fc1 / fc2-dgrad and the
-    // wait for the first row costs more than the NVLink bytes it saves (A/B in
-    // DESIGN.md); MOE_DISPATCH_DEDUP=1 turns it on for link-bound configurations
-    L->dedup = L->n > 1 && L->k > 1 && L->el > 1 && getenv("MOE_DISPATCH_DEDUP") != nullptr;
+    // on by default (DeepSeek shape, EP = 4: 9.17 -> 8.93 ms per step with the
+    // dynamic tile schedule; Mixtral EP = 4 unchanged); MOE_NO_DISPATCH_DEDUP=1 off
+    L->dedup = L->n > 1 && L->k > 1 && L->el > 1 && getenv("MOE_NO_DISPATCH_DEDUP") == nullptr;
     // zero the permuted buffers once so never-written rows are finite
     cudaMemset(L->x_perm, 0, Mp * h * 2);
     cudaMemset(L->dy_perm, 0, Mp * h * 2);

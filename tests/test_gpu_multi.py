@@ -45,12 +45,12 @@ def test_ep2_several_experts_per_token_on_a_rank(dedup):
     experts (the dispatch dedup path when enabled); >= 256 rows per expert, so
     CTA-pair tiles with M=128 tails."""
     env = {"MP_CF": "0", "MP_E": "8", "MP_K": "4", "MP_TR": "256"}
-    if dedup == "1":
-        env["MOE_DISPATCH_DEDUP"] = "1"
+    if dedup == "0":
+        env["MOE_NO_DISPATCH_DEDUP"] = "1"
     _run(2, env)
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
 def test_ep4_fine_grained_dedup():
     """DeepSeek-style routing at small scale: E = 32, k = 8, EP = 4, dedup on, drops."""
-    _run(4, {"MP_CF": "1.25", "MP_E": "32", "MP_K": "8", "MP_TR": "256", "MOE_DISPATCH_DEDUP": "1"})
+    _run(4, {"MP_CF": "1.25", "MP_E": "32", "MP_K": "8", "MP_TR": "256"})
