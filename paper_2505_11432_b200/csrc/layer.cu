@@ -711,7 +711,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     }
     L->mark(PH_DGATE, s);
     if (!L->gate_after) {
-        dgate_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgate_part, (int)(f / 256) * 2, L->row_dst,
+        dgate_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->dgate_part, (int)(f / 256) * 2, L->row_dst,
                                                     L->gpad_off + el, L->tab<float>(F_DGATE));
         count_launch();
     }

@@ -340,13 +340,19 @@ static __global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int 
 static __global__ void dgate_reduce_kernel(const float* __restrict__ part, int n_parts,
                                     const int32_t* __restrict__ row_dst, const int32_t* nrows_pad,
                                     float* const* __restrict__ dst_bufs) {
+    // one warp per row: coalesced reads of the row's partials, fixed-order
+    // lane sums then a butterfly (deterministic)
     const int total = *nrows_pad;
-    for (int pp = blockIdx.x * blockDim.x + threadIdx.x; pp < total; pp += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int pp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pp < total; pp += nw) {
         const int d = row_dst[pp];
         if (d < 0) continue;
         float s = 0.0f;
-        for (int q = 0; q < n_parts; ++q) s += part[(int64_t)pp * n_parts + q];
-        dst_bufs[d >> 27][d & ((1 << 27) - 1)] = s;
+        for (int q = lane; q < n_parts; q += 32) s += part[(int64_t)pp * n_parts + q];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) dst_bufs[d >> 27][d & ((1 << 27) - 1)] = s;
     }
 }
 
@@ -396,7 +402,7 @@ static __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part
 }
 
 // Pack w1 [el][2f][h] ([a | b] rows) into the interleaved layout the fused
-// SwiGLU epilogue expects: per 256-row block, 128 a-rows then 128 b-rows.
+// SwiGLU epilogue expects: per 128-row block, 64 a-rows then 64 b-rows.
 static __global__ void pack_w1_kernel(const uint16_t* __restrict__ w1, uint16_t* __restrict__ w1p, int el,
                                int f, int h) {
     const int64_t rows = (int64_t)el * 2 * f;
