@@ -66,7 +66,8 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     const int grid = p.grid > 0 ? p.grid : kNumSMs;
     GemmArgs a = args;
     static const bool static_tiles = getenv("MOE_STATIC_TILES") != nullptr;
-    if (!a.tile_counter && !static_tiles && !p.k_grouped) {
+    // (the kernel keeps the static stride for K-grouped and K >= 8192 GEMMs)
+    if (!a.tile_counter && !static_tiles && !p.k_grouped && a.K < 8192) {
         int dev = 0;
         MOE_CUDA_TRY(cudaGetDevice(&dev));
         a.tile_counter = tile_counter_slot(dev);

@@ -26,6 +26,8 @@
 //                   overlaps tile i+1's MMA.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace moe {
@@ -791,7 +793,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     // tile costs uneven, and a drifting static stride breaks the L2 sharing of
     // weight panels: 2.3x DRAM reads measured); the K-grouped wgrads keep the
     // static stride, which measured faster for them
-    const bool dyn = !K_GROUPED && args.tile_counter != nullptr;
+    // long-K M-grouped GEMMs (K >= 8192: the Mixtral fc2 / fc1 dgrad) keep the
+    // single-lane issue and the static stride: there the faster warp-convergent
+    // issue and the dynamic schedule raised DRAM re-reads (fc1 dgrad: 3.0 GB ->
+    // 5.2 / 8.5 GB, ncu) and, under the power cap, the time
+    const bool legacy = !K_GROUPED && args.K >= 8192;
+    const bool dyn = !K_GROUPED && !legacy && args.tile_counter != nullptr;
     // i-th tile of this CTA (pair): static stride, or dynamic. The leader's
     // producer fetches (atomic, in order) and publishes to the local queue and,
     // for a pair, to the peer's; every other role dequeues. -1 ends the loop.
@@ -848,8 +855,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
 
     if (warp == 0) {
         // ===================== TMA producer =====================
-        // whole warp in convergence, one elected lane issues (as for the MMA)
-        {
+        // CONV: whole warp in convergence, one elected lane issues (as for the
+        // MMA); otherwise lane 0 alone (long-K GEMMs, see `legacy`)
+        auto producer = [&](auto conv_tag) {
+            constexpr bool CONV = decltype(conv_tag)::value;
             int stage = 0;
             uint32_t phase = 0;
             const int arow = (int)cta_rank * BM;       // this CTA's A rows within the tile
@@ -866,13 +875,22 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                     uint32_t fb_leader = 0;
                     if (CG == 2) {
                         fb_leader = map_to_cta(fb, 0);
-                        if (leader) mbar_arrive_expect_tx_warp(fb, CG * Cfg::STAGE_BYTES);
+                        if (leader) {
+                            if (CONV) mbar_arrive_expect_tx_warp(fb, CG * Cfg::STAGE_BYTES);
+                            else mbar_arrive_expect_tx(fb, CG * Cfg::STAGE_BYTES);
+                        }
                     } else {
-                        mbar_arrive_expect_tx_warp(fb, Cfg::STAGE_BYTES);
+                        if (CONV) mbar_arrive_expect_tx_warp(fb, Cfg::STAGE_BYTES);
+                        else mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES);
                     }
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
-                        if (CG == 2) tma_load_2d_2sm_warp(dst, map, fb_leader, c0, c1);
-                        else tma_load_2d_warp(dst, map, fb, c0, c1);
+                        if (CONV) {
+                            if (CG == 2) tma_load_2d_2sm_warp(dst, map, fb_leader, c0, c1);
+                            else tma_load_2d_warp(dst, map, fb, c0, c1);
+                        } else {
+                            if (CG == 2) tma_load_2d_2sm(dst, map, fb_leader, c0, c1);
+                            else tma_load_2d(dst, map, fb, c0, c1);
+                        }
                     };
                     if (!K_GROUPED) {
                         if (DISPATCH && kb == 0) {
@@ -890,7 +908,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                                         }
                                     }
                             }
-                            __syncwarp();
+                            if (CONV) __syncwarp();
                             fence_proxy_async_global();   // every lane: the issuing lane is elected
                         }
                         // half tile: each CTA of the pair takes 64 rows (the box's other
@@ -919,13 +937,19 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
+        };
+        if (legacy) {
+            if (lane == 0) producer(std::false_type{});
+        } else {
+            producer(std::true_type{});
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
         // The whole warp walks the tile / k-block sequence in convergence, so
         // descriptors and TMEM addresses stay warp-uniform (uniform registers)
         // and one elected lane issues: no per-MMA register broadcast loops.
-        if (leader) {
+        auto mma_role = [&](auto conv_tag) {
+            constexpr bool CONV = decltype(conv_tag)::value;
             constexpr uint32_t idesc_full = make_idesc(TILE_M, BN, 1, A_MN, B_MN);
             constexpr uint32_t idesc_half = make_idesc(128, BN, 1, A_MN, B_MN);
             // stage s's descriptors = stage 0's + s * STAGE_BYTES / 16 (14-bit
@@ -958,16 +982,38 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t ad = ad0 + kk * a_kstep, bd = bd0 + kk * b_kstep;
-                        if (CG == 2) umma_bf16_2sm_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-                        else umma_bf16_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        if (CONV) {
+                            if (CG == 2) umma_bf16_2sm_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                            else umma_bf16_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        } else {
+                            if (CG == 2) umma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                            else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        }
                     }
-                    if (CG == 2) umma_commit_2sm_mc_warp(&empty_bar[stage]);
-                    else umma_commit_warp(&empty_bar[stage]);
+                    if (CONV) {
+                        if (CG == 2) umma_commit_2sm_mc_warp(&empty_bar[stage]);
+                        else umma_commit_warp(&empty_bar[stage]);
+                    } else {
+                        if (CG == 2) umma_commit_2sm_mc(&empty_bar[stage]);
+                        else umma_commit(&empty_bar[stage]);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if (CG == 2) umma_commit_2sm_mc_warp(&tfull_bar[acc]);
-                else umma_commit_warp(&tfull_bar[acc]);
+                if (CONV) {
+                    if (CG == 2) umma_commit_2sm_mc_warp(&tfull_bar[acc]);
+                    else umma_commit_warp(&tfull_bar[acc]);
+                } else {
+                    if (CG == 2) umma_commit_2sm_mc(&tfull_bar[acc]);
+                    else umma_commit(&tfull_bar[acc]);
+                }
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        };
+        if (leader) {
+            if (legacy) {
+                if (lane == 0) mma_role(std::false_type{});
+            } else {
+                mma_role(std::true_type{});
             }
         }
     } else if (DISPATCH && warp >= 2 + Cfg::EPI_WARPS) {

@@ -14,6 +14,7 @@ def _rel(a, b):
 @pytest.mark.parametrize("rows_per_group,N,K,bn", [
     ([128], 256, 64, 256), ([128], 256, 512, 256), ([256, 128, 384], 512, 1024, 256),
     ([128, 0, 256], 256, 256, 256), ([128] * 4, 384, 320, 128), ([512, 640], 1024, 4096, 256),
+    ([256, 384], 512, 8192, 256),   # K >= 8192: single-lane issue, static stride
 ])
 @pytest.mark.parametrize("cta_pair", [False, True])
 def test_m_grouped_kmajor(rows_per_group, N, K, bn, cta_pair):
@@ -39,7 +40,8 @@ def test_m_grouped_kmajor(rows_per_group, N, K, bn, cta_pair):
             off += r
 
 
-@pytest.mark.parametrize("rows_per_group,N,K", [([128], 256, 64), ([256, 128], 512, 768), ([512, 384], 256, 512)])
+@pytest.mark.parametrize("rows_per_group,N,K", [([128], 256, 64), ([256, 128], 512, 768), ([512, 384], 256, 512),
+                                                 ([384, 256], 256, 8192)])
 @pytest.mark.parametrize("cta_pair", [False, True])
 def test_m_grouped_b_mnmajor(rows_per_group, N, K, cta_pair):
     from paper_2505_11432_b200 import ops
