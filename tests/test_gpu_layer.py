@@ -172,3 +172,31 @@ def test_layer_with_fused_rmsnorm():
     assert rel(L.norm_grad().cpu().numpy(), odg) < TOL
     assert rel(dw1.float().cpu().numpy(), ob["dw1"]) < TOL
     assert rel(dwr.cpu().numpy(), ob["dwr"]) < TOL
+
+
+@pytest.mark.parametrize("T,E,k", [(512, 8, 2), (1024, 8, 2)])
+def test_layer_experts_without_tokens(T, E, k):
+    """Injected routing that leaves experts 3..E-1 empty: empty groups in the
+    M-grouped GEMMs (no tiles) and empty contractions in the wgrads (dW exactly
+    zero); at T=1024 the busy experts exceed 256 rows (CTA-pair tiles + tails)."""
+    import pyoracle as P
+    h, f = 512, 512
+    L, x, w1, w2, wr = make_layer(T, h, f, E, k, seed=9, route_mode="injected")
+    rng = np.random.default_rng(4)
+    ex = np.stack([rng.permutation(3)[:k] for _ in range(T)]).astype(np.int32)   # experts 0..2 only
+    gates = rng.random((T, k)).astype(np.float32)
+    gates /= gates.sum(1, keepdims=True)
+    L.set_routing(torch.from_numpy(ex).cuda(), torch.from_numpy(gates).cuda())
+    y = L.forward(x.cuda())
+    dy = (torch.randn(T, h, generator=torch.Generator().manual_seed(5)) * 0.1).bfloat16()
+    dx, dw1, dw2, _ = L.backward(dy.cuda())
+    torch.cuda.synchronize()
+    dr = np.zeros(T, np.uint8)
+    oy = P.orc_moe_forward(x.float().numpy(), ex, gates, dr, w1.float().numpy(), w2.float().numpy())
+    assert rel(y.float().cpu().numpy(), oy) < TOL
+    ob = P.orc_moe_backward(x.float().numpy(), dy.float().numpy(), ex, gates, np.zeros((T, E), np.float32),
+                            dr, w1.float().numpy(), w2.float().numpy(), wr.float().numpy())
+    assert rel(dw1.float().cpu().numpy()[:3], ob["dw1"][:3]) < TOL
+    assert rel(dw2.float().cpu().numpy()[:3], ob["dw2"][:3]) < TOL
+    assert dw1[3:].abs().max().item() == 0.0 and dw2[3:].abs().max().item() == 0.0
+    assert rel(L.routing()["dgates"].cpu().numpy(), ob["dgates"]) < TOL
