@@ -381,7 +381,8 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->first_row, L->T));
     TRY_ALLOC(dalloc(&L->dup_src, Mp));
     TRY_ALLOC(dalloc(&L->row_done, Mp));
-    TRY_ALLOC(dalloc(&L->rw_part, ((Tr + kRwChunk - 1) / kRwChunk) * L->E * h));
+    TRY_ALLOC(dalloc(&L->rw_part, (L->E <= 8 ? (Tr + kRw8Chunk - 1) / kRw8Chunk : (Tr + kRwChunk - 1) / kRwChunk) *
+                                      L->E * h));
     TRY_ALLOC(dalloc(&L->tab_remote, F_COUNT * L->n));
     TRY_ALLOC(dalloc(&L->tab_local, F_COUNT * L->n));
     TRY_ALLOC(dalloc(&L->err, 1));
@@ -781,15 +782,22 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
             a.ldo = h;
             MOE_TRY(gemm_launch(L->p_router_wgrad, a, s));
         } else if (router) {
-            const int nch = (int)((Tr + kRwChunk - 1) / kRwChunk);
-            if (L->E <= 8)
-                router_wgrad_partial_kernel<8><<<dim3((unsigned)((h + 255) / 256), nch), 256, 0, s>>>(
+            int nch;
+            if (L->E <= 8 && h % 8 == 0) {
+                nch = (int)((Tr + kRw8Chunk - 1) / kRw8Chunk);
+                router_wgrad_partial8_kernel<<<dim3((unsigned)((h / 8 + 127) / 128), nch), 128, 0, s>>>(
                     L->dlogits, L->mine<uint16_t>(F_X), (int)Tr, (int)h, (int)L->E, L->rw_part);
-            else
+            } else {
+                nch = (int)((Tr + kRwChunk - 1) / kRwChunk);
                 router_wgrad_partial_kernel<32><<<dim3((unsigned)((h + 255) / 256), nch), 256, 0, s>>>(
                     L->dlogits, L->mine<uint16_t>(F_X), (int)Tr, (int)h, (int)L->E, L->rw_part);
-            router_wgrad_reduce_kernel<<<kNumSMs * 2, 256, 0, s>>>(L->rw_part, nch, (int)L->E,
-                                                                   (int)h, d_dwr);
+            }
+            if ((L->E * h) % 4 == 0)
+                chunk_sum4_kernel<<<(unsigned)((L->E * h / 4 + 31) / 32), 256, 0, s>>>(L->rw_part, nch, L->E * h,
+                                                                                    d_dwr);
+            else
+                router_wgrad_reduce_kernel<<<kNumSMs * 2, 256, 0, s>>>(L->rw_part, nch, (int)L->E,
+                                                                       (int)h, d_dwr);
             count_launch(2);
         } else {
             MOE_CUDA_TRY(cudaMemsetAsync(d_dwr, 0, L->E * h * 4, s));

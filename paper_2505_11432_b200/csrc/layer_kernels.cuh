@@ -391,6 +391,59 @@ static __global__ void router_wgrad_partial_kernel(const float* __restrict__ dlo
     }
 }
 
+// E <= 8: 8 columns per thread (one 16 B load of x per token, the chunk's 32
+// tokens' loads in flight), token chunks of kRw8Chunk; same [chunk][E][h]
+// partial layout, summed in fixed chunk order by router_wgrad_reduce_kernel.
+constexpr int kRw8Chunk = 32;
+static __global__ void __launch_bounds__(128) router_wgrad_partial8_kernel(
+    const float* __restrict__ dlogits, const uint16_t* __restrict__ x, int T, int h, int E,
+    float* __restrict__ part) {
+    __shared__ float s_dl[kRw8Chunk * 8];
+    const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    const int t0 = blockIdx.y * kRw8Chunk;
+    const int nt = min(kRw8Chunk, T - t0);
+    for (int i = threadIdx.x; i < kRw8Chunk * 8; i += blockDim.x) {
+        const int tt = i >> 3, ee = i & 7;
+        s_dl[i] = (tt < nt && ee < E) ? dlogits[(int64_t)(t0 + tt) * E + ee] : 0.0f;
+    }
+    __syncthreads();
+    if (c0 >= h) return;
+    float acc[8][8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[q][j] = 0.0f;
+    const uint4* xp = reinterpret_cast<const uint4*>(x + (int64_t)t0 * h + c0);
+    const int hv = h / 8;
+#pragma unroll 1
+    for (int tt = 0; tt < kRw8Chunk; tt += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = tt + u < nt ? __ldg(xp + (int64_t)(tt + u) * hv) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float2 a = unpack_bf16x2(v[u].x), b = unpack_bf16x2(v[u].y), c = unpack_bf16x2(v[u].z),
+                         d = unpack_bf16x2(v[u].w);
+            const float xf[8] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y};
+            const float* dl = s_dl + (tt + u) * 8;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float g = dl[q];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[q][j] = fmaf(g, xf[j], acc[q][j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (q < E) {
+            float4* o = reinterpret_cast<float4*>(part + ((int64_t)blockIdx.y * E + q) * h + c0);
+            o[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+            o[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
+        }
+    }
+}
+
 static __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int nchunks, int E, int h,
                                            float* __restrict__ dwr) {
     const int64_t n = (int64_t)E * h;
@@ -398,6 +451,40 @@ static __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part
         float s = 0.0f;
         for (int q = 0; q < nchunks; ++q) s += part[(int64_t)q * n + i];
         dwr[i] = s;
+    }
+}
+
+// Same sum for many chunks (n % 4 == 0): a 256-thread block owns 32 float4
+// outputs; its 8 warps take every 8th chunk (8 loads in flight each) and the
+// 8 partial sums are added in warp order through shared memory (fixed order,
+// deterministic).
+static __global__ void __launch_bounds__(256) chunk_sum4_kernel(const float* __restrict__ part, int nchunks,
+                                                                 int64_t n, float* __restrict__ out) {
+    __shared__ float4 s_p[8][32];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int64_t n4 = n / 4;
+    const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+    const float4* p4 = reinterpret_cast<const float4*>(part);
+    float4 s = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (i < n4) {
+        for (int q0 = g; q0 < nchunks; q0 += 64) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + 8 * u;
+                v[u] = q < nchunks ? p4[(int64_t)q * n4 + i] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w; }
+        }
+    }
+    s_p[g][lane] = s;
+    __syncthreads();
+    if (g == 0 && i < n4) {
+        float4 t = s_p[0][lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) { t.x += s_p[w][lane].x; t.y += s_p[w][lane].y; t.z += s_p[w][lane].z; t.w += s_p[w][lane].w; }
+        reinterpret_cast<float4*>(out)[i] = t;
     }
 }
 
