@@ -66,8 +66,8 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     const int grid = p.grid > 0 ? p.grid : kNumSMs;
     GemmArgs a = args;
     static const bool static_tiles = getenv("MOE_STATIC_TILES") != nullptr;
-    // (the kernel keeps the static stride for K-grouped and K >= 8192 GEMMs)
-    if (!a.tile_counter && !static_tiles && !p.k_grouped && a.K < 8192) {
+    // (the kernel keeps the static stride for K-grouped and multi-group K >= 8192 GEMMs)
+    if (!a.tile_counter && !static_tiles && !p.k_grouped && (a.K < 8192 || a.G == 1)) {
         int dev = 0;
         MOE_CUDA_TRY(cudaGetDevice(&dev));
         a.tile_counter = tile_counter_slot(dev);

@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     // single-lane issue and the static stride: there the faster warp-convergent
     // issue and the dynamic schedule raised DRAM re-reads (fc1 dgrad: 3.0 GB ->
     // 5.2 / 8.5 GB, ncu) and, under the power cap, the time
-    const bool legacy = !K_GROUPED && args.K >= 8192;
+    const bool legacy = !K_GROUPED && args.K >= 8192 && G > 1;   // single-group GEMMs have no tails to drift on
     const bool dyn = !K_GROUPED && !legacy && args.tile_counter != nullptr;
     // i-th tile of this CTA (pair): static stride, or dynamic. The leader's
     // producer fetches (atomic, in order) and publishes to the local queue and,
