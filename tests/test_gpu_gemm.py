@@ -14,7 +14,8 @@ def _rel(a, b):
 @pytest.mark.parametrize("rows_per_group,N,K,bn", [
     ([128], 256, 64, 256), ([128], 256, 512, 256), ([256, 128, 384], 512, 1024, 256),
     ([128, 0, 256], 256, 256, 256), ([128] * 4, 384, 320, 128), ([512, 640], 1024, 4096, 256),
-    ([256, 384], 512, 8192, 256),   # K >= 8192: single-lane issue, static stride
+    ([256, 384], 512, 8192, 256),   # K >= 8192, several groups: single-lane issue, static stride
+    ([384], 512, 8192, 256),        # K >= 8192, one group: convergent issue, dynamic tiles
 ])
 @pytest.mark.parametrize("cta_pair", [False, True])
 def test_m_grouped_kmajor(rows_per_group, N, K, bn, cta_pair):
