@@ -223,7 +223,7 @@ moe_status moe_attn_gemm_rs(moe_attn* A, const uint16_t* d_o, uint16_t* d_y_shar
     a.rank_base = reinterpret_cast<void* const*>(A->tab + A->n);
     MOE_TRY(gemm_launch(p, a, s));
     MOE_TRY(attn_barrier(A, 2, s));
-    combine_reduce_kernel<false><<<kNumSMs * 4, 256, 0, s>>>(
+    launch_combine<false>(s, 
         A->arena + A->off_stage, nullptr, nullptr, (int)A->sr, (int)A->n, (int)A->h, d_y_shard,
         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     count_launch();

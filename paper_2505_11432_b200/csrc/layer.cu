@@ -619,11 +619,11 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     const uint8_t* drop_loc = L->dropped + L->rank * Tr;
     const float* slot_gate = L->gate_after ? L->gt_loc : nullptr;
     if (L->fp8)
-        combine_reduce_kernel<true><<<kNumSMs * 4, 256, 0, s>>>(
+        launch_combine<true>(s, 
             L->mine<uint8_t>(F_STAGE8), L->mine<float>(F_SSC), drop_loc, (int)Tr, (int)k, (int)h, d_y,
             slot_gate, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     else
-        combine_reduce_kernel<false><<<kNumSMs * 4, 256, 0, s>>>(
+        launch_combine<false>(s, 
             L->mine<uint16_t>(F_STAGE), nullptr, drop_loc, (int)Tr, (int)k, (int)h, d_y, slot_gate,
             nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     count_launch();
@@ -721,13 +721,13 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     const bool router = L->cfg.route_mode == 0;
     uint16_t* dx_moe = L->norm ? L->dxn : d_dx;  // gradient w.r.t. the (normalised) layer input
     if (L->fp8)
-        combine_reduce_kernel<true><<<kNumSMs * 4, 256, 0, s>>>(
+        launch_combine<true>(s, 
             L->mine<uint8_t>(F_DSTAGE8), L->mine<float>(F_DSSC), drop_loc, (int)Tr, (int)k, (int)h,
             dx_moe, nullptr, router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
             router ? dgate_sym : nullptr, router ? L->wr : nullptr, router ? L->dlogits : nullptr,
             (int)L->E);
     else
-        combine_reduce_kernel<false><<<kNumSMs * 4, 256, 0, s>>>(
+        launch_combine<false>(s, 
             L->mine<uint16_t>(F_DSTAGE), nullptr, drop_loc, (int)Tr, (int)k, (int)h, dx_moe, nullptr,
             router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr, router ? dgate_sym : nullptr,
             router ? L->wr : nullptr, router ? L->dlogits : nullptr, (int)L->E);
