@@ -41,6 +41,10 @@ CONFIGS = {
                              ffn_hidden=14336, num_experts=8, top_k=2, tokens_per_rank=4096,
                              comm="fp8", gate="after_fc2_out",
                              routing_fixture="tests/golden/routing_cfg5_zipf_nodrop_n8.npz"),
+    # FP8 communication with the learned router (uniform-ish load): the cost of the
+    # E4M3 quantise / dequantise against the halved NVLink bytes
+    "mixtral_fp8": dict(workload="mixtral-8x7b-moe-layer-fwd+bwd-fp8comm", hidden=4096, ffn_hidden=14336,
+                        num_experts=8, top_k=2, tokens_per_rank=4096, comm="fp8", gate="after_fc2_out"),
     # configs[3]: sequence-parallel attention QKV / out-proj, hidden 8192, seq 8192, GQA m=8
     "attn": dict(workload="sp-attention-qkv-ag-gemm+out-proj-gemm-rs", hidden=8192, seq=8192, gqa=8),
     # §8f row 3: Ulysses SP projections (the paper's attention strategy) at the
