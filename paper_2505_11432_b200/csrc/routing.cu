@@ -173,47 +173,101 @@ __global__ void permute_hist_kernel(const int32_t* __restrict__ experts,
         if (s_e[e]) atomicAdd(&per_expert_counts[e], s_e[e]);
 }
 
-// One CTA: column prefix per bin over chunks, then scan over bins.
+// Exclusive scan of a[0..n) in shared memory by the whole (1024-thread) block:
+// up to 4 consecutive items per thread, warp shuffles, then a scan of the 32
+// warp totals. Returns the total (to every thread).
+__device__ int block_exclusive_scan(int* a, int n, int* s_warp) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + blockDim.x - 1) / blockDim.x;   // items per thread (<= 4 used here)
+    const int beg = tid * per;
+    int loc[4] = {0, 0, 0, 0};
+    int sum = 0;
+    for (int q = 0; q < per && q < 4; ++q) {
+        loc[q] = beg + q < n ? a[beg + q] : 0;
+        sum += loc[q];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += u;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+        int wi = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += u;
+        }
+        s_warp[lane] = wi - w;           // exclusive warp offsets
+        if (lane == 31) s_warp[32] = wi;  // block total
+    }
+    __syncthreads();
+    int run = s_warp[warp] + incl - sum;
+    for (int q = 0; q < per && q < 4; ++q) {
+        if (beg + q < n) a[beg + q] = run;
+        run += loc[q];
+    }
+    const int total = s_warp[32];
+    __syncthreads();
+    return total;
+}
+
+// One CTA (1024 threads): column prefix per bin over chunks (8 chunk loads in
+// flight per thread), block scans over bins and over the padded expert sizes.
+// Same results as a serial scan (integer sums).
 __global__ void permute_scan_kernel(int* __restrict__ chunk_cnt, int nchunks, int nbins, int el,
                                     int n_src, int* __restrict__ expert_offsets,
                                     int* __restrict__ rows_out, int* __restrict__ group_pad_rows,
                                     int* __restrict__ group_pad_off, int pad) {
-    extern __shared__ int s_tot[];  // [nbins + 1]
+    extern __shared__ int s_tot[];  // [nbins + 1] then [el + 1] padded sizes
+    __shared__ int s_warp[33];
+    int* s_pad = s_tot + nbins + 1;
     for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
         int acc = 0;
-        for (int c = 0; c < nchunks; ++c) {
+        int c = 0;
+        for (; c + 8 <= nchunks; c += 8) {
+            int v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = chunk_cnt[(int64_t)(c + u) * nbins + b];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                chunk_cnt[(int64_t)(c + u) * nbins + b] = acc;  // exclusive within bin
+                acc += v[u];
+            }
+        }
+        for (; c < nchunks; ++c) {
             const int v = chunk_cnt[(int64_t)c * nbins + b];
-            chunk_cnt[(int64_t)c * nbins + b] = acc;  // exclusive within bin
+            chunk_cnt[(int64_t)c * nbins + b] = acc;
             acc += v;
         }
         s_tot[b] = acc;
     }
     __syncthreads();
+    const int total = block_exclusive_scan(s_tot, nbins, s_warp);
     if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int b = 0; b < nbins; ++b) {
-            const int v = s_tot[b];
-            s_tot[b] = acc;
-            acc += v;
-        }
-        s_tot[nbins] = acc;
-        *rows_out = acc;
-        int poff = 0;
-        for (int e = 0; e < el; ++e) {
-            const int beg = s_tot[e * n_src];
-            const int end = s_tot[(e + 1) * n_src];
-            expert_offsets[e] = beg;
-            if (group_pad_rows) {
-                const int pr = (end - beg + pad - 1) / pad * pad;
-                group_pad_rows[e] = pr;
-                group_pad_off[e] = poff;
-                poff += pr;
-            }
-        }
-        expert_offsets[el] = acc;
-        if (group_pad_off) group_pad_off[el] = poff;
+        s_tot[nbins] = total;
+        *rows_out = total;
     }
     __syncthreads();
+    for (int e = threadIdx.x; e < el; e += blockDim.x) {
+        const int beg = s_tot[e * n_src];
+        const int end = s_tot[(e + 1) * n_src];
+        expert_offsets[e] = beg;
+        s_pad[e] = (end - beg + pad - 1) / pad * pad;
+    }
+    if (threadIdx.x == 0) expert_offsets[el] = total;
+    __syncthreads();
+    if (group_pad_rows) {
+        for (int e = threadIdx.x; e < el; e += blockDim.x) group_pad_rows[e] = s_pad[e];
+        __syncthreads();
+        const int ptotal = block_exclusive_scan(s_pad, el, s_warp);
+        for (int e = threadIdx.x; e < el; e += blockDim.x) group_pad_off[e] = s_pad[e];
+        if (threadIdx.x == 0) group_pad_off[el] = ptotal;
+    }
     // add bin base to every chunk's exclusive offsets
     for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
         const int base = s_tot[b];
@@ -436,7 +490,7 @@ moe_status launch_permute(const int32_t* experts, const int32_t* src, const uint
                                                            (int)E, first, el, (int)n_src,
                                                            chunk_cnt, per_expert_counts);
     count_launch();
-    const size_t sm2 = sizeof(int) * (nbins + 1);
+    const size_t sm2 = sizeof(int) * (nbins + 1 + el + 1);
     permute_scan_kernel<<<1, 1024, sm2, s>>>(chunk_cnt, nchunks, nbins, el, (int)n_src,
                                              expert_offsets, rows, group_pad_rows, group_pad_off,
                                              pad);

@@ -10,19 +10,42 @@ namespace moe {
 
 __device__ __forceinline__ void topk_select(const float* lg, int E, int k, int32_t* ex,
                                             float* gt, int lane) {
-    // warp-parallel argmax rounds (k <= 8), ties -> lower expert id
+    // warp-parallel argmax rounds (k <= 8), ties -> lower expert id. For E <= 256
+    // each lane keeps its (up to 8) logits in registers and a taken-mask; the
+    // visiting order and comparisons are those of the generic loop below.
     float sel_val[8];
     int sel_id[8];
+    const bool regs = E <= 256;
+    float rv[8];
+    unsigned taken_mask = 0;
+    if (regs) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) rv[q] = (lane + 32 * q < E) ? lg[lane + 32 * q] : 0.0f;
+    }
     for (int j = 0; j < k; ++j) {
         float best = -INFINITY;
         int bid = 0x7fffffff;
-        for (int e = lane; e < E; e += 32) {
-            bool taken = false;
-            for (int i = 0; i < j; ++i) taken |= (sel_id[i] == e);
-            const float v = lg[e];
-            if (!taken && (v > best || (v == best && e < bid) || bid == 0x7fffffff)) {
-                best = v;
-                bid = e;
+        if (regs) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int e = lane + 32 * q;
+                if (e < E && !(taken_mask >> q & 1u)) {
+                    const float v = rv[q];
+                    if (v > best || (v == best && e < bid) || bid == 0x7fffffff) {
+                        best = v;
+                        bid = e;
+                    }
+                }
+            }
+        } else {
+            for (int e = lane; e < E; e += 32) {
+                bool taken = false;
+                for (int i = 0; i < j; ++i) taken |= (sel_id[i] == e);
+                const float v = lg[e];
+                if (!taken && (v > best || (v == best && e < bid) || bid == 0x7fffffff)) {
+                    best = v;
+                    bid = e;
+                }
             }
         }
 #pragma unroll
@@ -36,6 +59,7 @@ __device__ __forceinline__ void topk_select(const float* lg, int E, int k, int32
         }
         sel_val[j] = best;
         sel_id[j] = bid;
+        if (regs && bid != 0x7fffffff && (bid & 31) == lane) taken_mask |= 1u << (bid >> 5);
     }
     if (lane == 0) {
         // gates = softmax over the k selected logits (max-subtracted, fp32)
