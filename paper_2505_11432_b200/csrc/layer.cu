@@ -190,9 +190,12 @@ moe_status build_plans(moe_layer* L) {
     if (L->gemm_router) {
         L->p_router = GemmPlan{};
         L->p_router.epi = EPI_STORE_F32;
-        L->p_router.cg = (L->Tr % 256 == 0) ? 2 : 1;
+        // only T_r/128 x E/128 output tiles: single-CTA 128 x 128 tiles keep
+        // 4x more SMs busy than 256 x 256 pairs (E = 256: 49 -> ~20 us)
+        L->p_router.bn = 128;
+        L->p_router.cg = 1;
         MOE_TRY(tmap_kmajor(&L->p_router.ta, L->arena + L->off[F_X], L->Tr, h, 128));
-        MOE_TRY(tmap_kmajor(&L->p_router.tb, L->wr, L->E, h, 256 / L->p_router.cg));
+        MOE_TRY(tmap_kmajor(&L->p_router.tb, L->wr, L->E, h, 128));
         const int32_t rr = (int32_t)L->Tr;
         MOE_CUDA_TRY(cudaMemcpy(L->router_rows, &rr, sizeof(rr), cudaMemcpyHostToDevice));
     }
