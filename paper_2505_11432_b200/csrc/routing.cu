@@ -144,13 +144,15 @@ __global__ void capacity_drop_kernel(const int32_t* __restrict__ experts, int T,
 //   2. one CTA scans (bin-major, chunk-minor) -> chunk offsets; expert offsets
 //   3. per-chunk stable scatter: warp match_any ranks + cross-warp prefix
 constexpr int kPermThreads = 256;
-constexpr int kPermChunk = 1024;  // entries per chunk (4 rounds of 256)
+// entries per chunk (multiple of kPermThreads): small problems use 256 so that
+// the histogram / scatter passes spread over more CTAs (Mixtral N=1: 8 -> 32)
+static int perm_chunk(int64_t n_ent) { return n_ent <= 65536 ? 256 : 1024; }
 
 __global__ void permute_hist_kernel(const int32_t* __restrict__ experts,
                                     const int32_t* __restrict__ src,
                                     const uint8_t* __restrict__ dropped, int T, int k, int E,
                                     int first, int el, int n_src, int* __restrict__ chunk_cnt,
-                                    int* __restrict__ per_expert_counts) {
+                                    int* __restrict__ per_expert_counts, int chunk) {
     extern __shared__ int s_h[];  // [nbins] then [E]
     const int nbins = el * n_src;
     int* s_e = s_h + nbins;
@@ -158,8 +160,8 @@ __global__ void permute_hist_kernel(const int32_t* __restrict__ experts,
     for (int e = threadIdx.x; e < E; e += blockDim.x) s_e[e] = 0;
     __syncthreads();
     const int64_t n_ent = (int64_t)T * k;
-    const int64_t beg = (int64_t)blockIdx.x * kPermChunk;
-    for (int64_t i = beg + threadIdx.x; i < beg + kPermChunk && i < n_ent; i += blockDim.x) {
+    const int64_t beg = (int64_t)blockIdx.x * chunk;
+    for (int64_t i = beg + threadIdx.x; i < beg + chunk && i < n_ent; i += blockDim.x) {
         const int t = (int)(i / k);
         if (dropped && dropped[t]) continue;
         const int e = experts[i];
@@ -289,7 +291,7 @@ __global__ void permute_scatter_kernel(const int32_t* __restrict__ experts,
                                        const int32_t* __restrict__ src,
                                        const uint8_t* __restrict__ dropped, int T, int k,
                                        int first, int el, int n_src,
-                                       const int* __restrict__ chunk_off, PermuteOut out) {
+                                       const int* __restrict__ chunk_off, PermuteOut out, int chunk) {
     extern __shared__ int s_w[];  // [8 warps][nbins] then running[nbins]
     const int nbins = el * n_src;
     int* s_run = s_w + 8 * nbins;
@@ -300,8 +302,8 @@ __global__ void permute_scatter_kernel(const int32_t* __restrict__ experts,
     }
     __syncthreads();
     const int64_t n_ent = (int64_t)T * k;
-    const int64_t beg = (int64_t)blockIdx.x * kPermChunk;
-    for (int round = 0; round < kPermChunk / kPermThreads; ++round) {
+    const int64_t beg = (int64_t)blockIdx.x * chunk;
+    for (int round = 0; round < chunk / kPermThreads; ++round) {
         const int64_t i = beg + round * kPermThreads + threadIdx.x;
         int bin = -1, e = -1, t = 0;
         if (i < n_ent) {
@@ -460,7 +462,7 @@ moe_status launch_capacity_drop(const int32_t* experts, int64_t T, int64_t E, in
 }
 
 size_t permute_workspace_bytes(int64_t T, int64_t E, int64_t k, int64_t n_src) {
-    const int64_t nchunks = (T * k + kPermChunk - 1) / kPermChunk;
+    const int64_t nchunks = (T * k + perm_chunk(T * k) - 1) / perm_chunk(T * k);
     return (size_t)std::max<int64_t>(nchunks, 1) * (size_t)(E * n_src) * sizeof(int) + 256;
 }
 
@@ -480,7 +482,8 @@ moe_status launch_permute(const int32_t* experts, const int32_t* src, const uint
     const int nbins = el * (int)n_src;
     MOE_CHECK_ARG(nbins <= 4096, "permute supports (E/n)*n_src <= 4096 bins");
     const int64_t n_ent = T * k;
-    const int nchunks = (int)std::max<int64_t>((n_ent + kPermChunk - 1) / kPermChunk, 1);
+    const int chunk = perm_chunk(n_ent);
+    const int nchunks = (int)std::max<int64_t>((n_ent + chunk - 1) / chunk, 1);
     int* chunk_cnt = static_cast<int*>(workspace);
     MOE_CUDA_TRY(cudaMemsetAsync(per_expert_counts, 0, sizeof(int32_t) * E, s));
     const size_t sm1 = sizeof(int) * (nbins + E);
@@ -488,7 +491,7 @@ moe_status launch_permute(const int32_t* experts, const int32_t* src, const uint
         MOE_CUDA_TRY(cudaFuncSetAttribute(permute_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
     permute_hist_kernel<<<nchunks, kPermThreads, sm1, s>>>(experts, src, dropped, (int)T, (int)k,
                                                            (int)E, first, el, (int)n_src,
-                                                           chunk_cnt, per_expert_counts);
+                                                           chunk_cnt, per_expert_counts, chunk);
     count_launch();
     const size_t sm2 = sizeof(int) * (nbins + 1 + el + 1);
     permute_scan_kernel<<<1, 1024, sm2, s>>>(chunk_cnt, nchunks, nbins, el, (int)n_src,
@@ -501,7 +504,7 @@ moe_status launch_permute(const int32_t* experts, const int32_t* src, const uint
         MOE_CUDA_TRY(cudaFuncSetAttribute(permute_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
     permute_scatter_kernel<<<nchunks, kPermThreads, sm3, s>>>(experts, src, dropped, (int)T,
                                                               (int)k, first, el, (int)n_src,
-                                                              chunk_cnt, po);
+                                                              chunk_cnt, po, chunk);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;
