@@ -35,7 +35,8 @@ def make_layer(T, h, f, E, k, seed=0, route_mode="learned", cf=0.0, gate_order="
 
 @pytest.mark.parametrize("T,h,f,E,k", [(256, 512, 512, 8, 2), (384, 768, 1024, 4, 1), (512, 512, 768, 16, 4),
                                        (512, 512, 256, 128, 8),    # fine-grained: GEMM router, 128-row tiles
-                                       (512, 512, 256, 256, 8)])   # + tensor-core router weight gradient
+                                       (512, 512, 256, 256, 8),    # + tensor-core router weight gradient
+                                       (512, 512, 4096, 4, 2)])    # fc1 dgrad K = 2f = 8192: single-lane issue, static tiles
 def test_layer_fwd_bwd_vs_oracle(T, h, f, E, k):
     import pyoracle as P
     L, x, w1, w2, wr = make_layer(T, h, f, E, k)
