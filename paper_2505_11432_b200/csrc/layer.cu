@@ -740,7 +740,10 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         const int nch = (int)((Tr + kRwChunk - 1) / kRwChunk);
         rmsnorm_dgamma_partial_kernel<<<dim3((unsigned)((h + 255) / 256), nch), 256, 0, s>>>(
             L->x_res, L->rstd, L->dxn, (int)Tr, (int)h, L->dgamma_part);
-        router_wgrad_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgamma_part, nch, 1, (int)h, L->dgamma);
+        if (h % 4 == 0)
+            chunk_sum4_kernel<<<(unsigned)((h / 4 + 31) / 32), 256, 0, s>>>(L->dgamma_part, nch, h, L->dgamma);
+        else
+            router_wgrad_reduce_kernel<<<kNumSMs, 256, 0, s>>>(L->dgamma_part, nch, 1, (int)h, L->dgamma);
         count_launch(3);
     }
     // dx is final here: callers may start its device->host copy while the
