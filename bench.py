@@ -259,6 +259,8 @@ def run_ours(args, cfg):
     x = (torch.randn(Tr, h, device="cuda", generator=gx) * 0.5).bfloat16()
     dy = (torch.randn(Tr, h, device="cuda", generator=gx) * 0.1).bfloat16()
     L.input_buffer.copy_(x)
+    L.dy_buffer.copy_(dy)          # inputs resident in the layer's own (symmetric) buffers
+    dy = L.dy_buffer
     dx = torch.empty(Tr, h, dtype=torch.bfloat16, device="cuda")
     dw1 = torch.empty(el, 2 * f, h, dtype=torch.bfloat16, device="cuda")
     dw2 = torch.empty(el, h, f, dtype=torch.bfloat16, device="cuda")

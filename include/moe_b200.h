@@ -207,6 +207,10 @@ const float* moe_layer_norm_grad(moe_layer* L);
  * residual stream when ffn_norm = 1, else the symmetric buffer peers read). A
  * caller may write x there directly and pass NULL as d_x to forward. */
 uint16_t* moe_layer_input_buffer(moe_layer* L);
+/* Device pointer of the layer's symmetric output-gradient buffer [T_r, h] bf16
+ * (peers pull dy rows from it). A caller may write dy there directly and pass
+ * this pointer as d_dy to backward: no copy. */
+uint16_t* moe_layer_dy_buffer(moe_layer* L);
 
 /* Injected routing (route_mode = 1): experts [T_r, k] int32, gates [T_r, k]
  * fp32 for this rank's tokens. */

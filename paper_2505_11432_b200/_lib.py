@@ -44,6 +44,7 @@ def lib() -> C.CDLL:
         L.moe_permute_workspace_size.restype = C.c_size_t
         L.moe_permute_workspace_size.argtypes = [C.c_int64] * 4
         for name, res, args in (("moe_layer_input_buffer", C.c_void_p, [C.c_void_p]),
+                                ("moe_layer_dy_buffer", C.c_void_p, [C.c_void_p]),
                                 ("moe_layer_ipc_handle_size", C.c_size_t, []),
                                 ("moe_layer_destroy", None, [C.c_void_p])):
             if hasattr(L, name):

@@ -467,6 +467,8 @@ uint16_t* moe_layer_input_buffer(moe_layer* L) {
     return L ? (L->norm ? L->x_res : L->mine<uint16_t>(F_X)) : nullptr;
 }
 
+uint16_t* moe_layer_dy_buffer(moe_layer* L) { return L ? L->mine<uint16_t>(F_DY) : nullptr; }
+
 moe_status moe_layer_set_norm_weight(moe_layer* L, const float* d_gamma, moe_stream_t stream) {
     MOE_CHECK_ARG(L && d_gamma, "null argument");
     MOE_CHECK_ARG(L->norm, "layer created without ffn_norm");

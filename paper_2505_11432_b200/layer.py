@@ -65,6 +65,8 @@ class MoELayer:
         check(lib().moe_layer_create(C.byref(cfg), C.byref(h_)))
         self._h = h_
         self._x_in = _view(lib().moe_layer_input_buffer(self._h), (tokens_per_rank, hidden), torch.bfloat16)
+        # symmetric dy buffer: writing dy here and passing it to backward skips a copy
+        self.dy_buffer = _view(lib().moe_layer_dy_buffer(self._h), (tokens_per_rank, hidden), torch.bfloat16)
 
     def __del__(self):
         h = getattr(self, "_h", None)
