@@ -5,8 +5,11 @@
  * (OpKind, /root/reference/proj/core/include/moeplan/simsched.hpp:32-44;
  * node names, core/src/graph.cpp:254-311) plus the routing-map functions the
  * reference implements on the CPU (core/include/moeplan/routing.hpp:49-106)
- * and the FP8 communication quantiser (numerics.hpp:61-62). Each declaration
- * names the reference interface it replaces.
+ * and the FP8 communication quantiser (numerics.hpp:61-62), the reference's
+ * numerics (round_to / quantize / emulate_reduce), the attention projections
+ * of both strategies (TP: ag_attn_in/rs_attn_out, SP/Ulysses: a2a_qkv /
+ * a2a_attn_out) and the compressed DP gradient sync (dp_sync_time). Each
+ * declaration names the reference interface it replaces.
  *
  * Conventions
  *   - plain pointers + explicit sizes; "d_" = device pointer, "h_" = host;
