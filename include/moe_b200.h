@@ -277,6 +277,14 @@ moe_status moe_layer_set_fused_dispatch(moe_layer* L, int fused);
 
 /* Non-zero if a cross-GPU flag wait of this layer timed out (synchronous). */
 int moe_layer_error_flag(moe_layer* L);
+/* Synchronises `stream` and returns MOE_ERR_TIMEOUT if a bounded cross-GPU
+ * wait (flag barrier or fused-dispatch row arrival) of this layer gave up
+ * since creation or the last moe_layer_clear_error; MOE_OK otherwise.
+ * forward / backward also return MOE_ERR_TIMEOUT on entry once an earlier
+ * call's timeout has reached the host (the flag is mirrored into pinned host
+ * memory at the end of every multi-GPU forward / backward). */
+moe_status moe_layer_status(moe_layer* L, moe_stream_t stream);
+moe_status moe_layer_clear_error(moe_layer* L);
 
 /* Generic grouped GEMM (reference OpKind::grouped_gemm): see gemm.h.
  * M-grouped: every group's row count is a multiple of 128 (also with cta_pair: a
@@ -285,6 +293,26 @@ moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b, void* d_d,
                             const int32_t* d_group_rows, int64_t total_rows, int64_t M, int64_t N,
                             int64_t K, int32_t a_mn_major, int32_t b_mn_major, int32_t k_grouped,
                             int32_t out_f32, int32_t bn, int32_t cta_pair, moe_stream_t stream);
+
+/* The layer's FP8 communication quantisers on their own (test / A-B hooks;
+ * the layer calls the same kernels):
+ *  - moe_quantize_e4m3_fast: the source-side quantiser of the dispatch
+ *    payloads, group 0 = per-token (forward x), 128 = grouped-128 (backward
+ *    dy). bf16 rows [rows, cols] -> codes [rows, cols] + fp32 scales.
+ *  - moe_grouped_gemm_e4m3: the fc2 / fc1-dgrad epilogue that quantises the
+ *    fp32 accumulators grouped-128 (combine payloads): M-grouped GEMM as in
+ *    moe_grouped_gemm, output row r -> codes [total_rows, N] + scales
+ *    [total_rows, N/128].
+ * Codes equal the reference quantize (numerics.cpp:113-160: scale =
+ * absmax/448 and x/scale in binary64, RNE to E4M3, saturation at 448) bit for
+ * bit on the same fp32/bf16 inputs; scales are the binary64 scale rounded once
+ * to fp32. */
+moe_status moe_quantize_e4m3_fast(const uint16_t* d_x, int64_t rows, int64_t cols, int32_t group,
+                                  uint8_t* d_codes, float* d_scales, moe_stream_t stream);
+moe_status moe_grouped_gemm_e4m3(const uint16_t* d_a, const uint16_t* d_b, uint8_t* d_codes,
+                                 float* d_scales, int32_t groups, const int32_t* d_group_rows,
+                                 int64_t total_rows, int64_t N, int64_t K, int32_t b_mn_major,
+                                 int32_t cta_pair, moe_stream_t stream);
 
 /* ===================================================================== */
 /* Multi-GPU fabric (NVLink P2P over NVSwitch; one process per GPU)       */
@@ -341,6 +369,8 @@ size_t moe_attn_ipc_handle_size(void);
 moe_status moe_attn_ipc_export(moe_attn* A, void* h_blob);
 moe_status moe_attn_ipc_import(moe_attn* A, const void* h_blobs);
 int moe_attn_error_flag(moe_attn* A);
+/* Synchronises `stream`; MOE_ERR_TIMEOUT if a cross-GPU wait gave up. */
+moe_status moe_attn_status(moe_attn* A, moe_stream_t stream);
 
 /* ===================================================================== */
 /* Ulysses sequence-parallel attention projections (replicated weights)     */
@@ -377,6 +407,8 @@ size_t moe_ulysses_ipc_handle_size(void);
 moe_status moe_ulysses_ipc_export(moe_ulysses* U, void* h_blob);
 moe_status moe_ulysses_ipc_import(moe_ulysses* U, const void* h_blobs);
 int moe_ulysses_error_flag(moe_ulysses* U);
+/* Synchronises `stream`; MOE_ERR_TIMEOUT if a cross-GPU wait gave up. */
+moe_status moe_ulysses_status(moe_ulysses* U, moe_stream_t stream);
 
 /* ===================================================================== */
 /* DP gradient sync with BF16 communication compression                    */
@@ -408,6 +440,8 @@ size_t moe_dp_ipc_handle_size(void);
 moe_status moe_dp_ipc_export(moe_dp* D, void* h_blob);
 moe_status moe_dp_ipc_import(moe_dp* D, const void* h_blobs);
 int moe_dp_error_flag(moe_dp* D);
+/* Synchronises `stream`; MOE_ERR_TIMEOUT if a cross-GPU wait gave up. */
+moe_status moe_dp_status(moe_dp* D, moe_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -393,11 +393,11 @@ void orc_moe_backward(const float* x, const float* dy, const int32_t* experts,
                         fc2in_all[(i * k + j) * f + q] = (float)fc2_in[q];
                     }
                     if (!gate_after) dg[j] += sg;
-                    for (int64_t c = 0; c < h; ++c) {
-                        double acc = 0.0;
-                        for (int64_t q = 0; q < 2 * f; ++q)
-                            acc += (double)dfc1[q] * (double)w1e[q * h + c];
-                        dxa[c] += acc;
+                    /* dx += W1e^T dfc1, row by row (contiguous in W1e) */
+                    for (int64_t q = 0; q < 2 * f; ++q) {
+                        const double d = dfc1[q];
+                        const float* w = w1e + q * h;
+                        for (int64_t c = 0; c < h; ++c) dxa[c] += d * (double)w[c];
                     }
                 }
                 /* router: gates = softmax over selected logits */
@@ -463,4 +463,193 @@ void orc_moe_backward(const float* x, const float* dy, const int32_t* experts,
             }
     }
     free(dfc1_all); free(fc2in_all); free(dout_all); free(dlog_all);
+}
+
+/* ------------------------------------------------------------------ */
+/* bf16-input restatement for full-shape sampled parity                 */
+/* ------------------------------------------------------------------ */
+/* The same math as orc_moe_forward / orc_moe_backward above, reading the
+ * bf16 tensors the GPU holds (uint16 bit patterns widened exactly to fp32)
+ * so full-size weights (DeepSeek shape: 22 GB of bf16) need not be widened
+ * on the host. Accumulation in binary64, rows contiguous in the weights. */
+
+static inline double bf2d(uint16_t u) {
+    union { uint32_t u; float f; } v;
+    v.u = (uint32_t)u << 16;
+    return (double)v.f;
+}
+
+static double dot_bd(const double* a, const uint16_t* b, int64_t n) {
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    int64_t i = 0;
+    for (; i + 4 <= n; i += 4) {
+        s0 += a[i] * bf2d(b[i]);
+        s1 += a[i + 1] * bf2d(b[i + 1]);
+        s2 += a[i + 2] * bf2d(b[i + 2]);
+        s3 += a[i + 3] * bf2d(b[i + 3]);
+    }
+    for (; i < n; ++i) s0 += a[i] * bf2d(b[i]);
+    return (s0 + s1) + (s2 + s3);
+}
+
+/* y, dx and dgates of the sampled tokens (graph.cpp:288-296 forward,
+ * :333-401 backward; gates = softmax over the selected logits, so the
+ * router term of dx is W_r^T dlogits with dlogits_e = g_e (dg_e - sum g dg)).
+ * x[T,h], dy[T,h] (may be NULL: forward only), w1[E,2f,h] ([a|b] rows),
+ * w2[E,h,f], wr[E,h] (may be NULL: no router term) are bf16 bit patterns.
+ * Outputs y[nt,h], dx[nt,h], dgates[nt,k] (dx/dgates ignored when dy NULL). */
+void orc_moe_rows_bf16(const uint16_t* x, const uint16_t* dy, const int32_t* experts,
+                       const float* gates, const uint8_t* dropped, const uint16_t* w1,
+                       const uint16_t* w2, const uint16_t* wr, int64_t h, int64_t f, int64_t E,
+                       int64_t k, int gate_after, const int64_t* tokens, int64_t nt, float* y,
+                       float* dx, float* dgates) {
+#pragma omp parallel
+    {
+        double* xt = (double*)malloc(sizeof(double) * (size_t)h);
+        double* dyt = (double*)malloc(sizeof(double) * (size_t)h);
+        double* fc1 = (double*)malloc(sizeof(double) * (size_t)(2 * f));
+        double* fc2_in = (double*)malloc(sizeof(double) * (size_t)f);
+        double* out = (double*)malloc(sizeof(double) * (size_t)h);
+        double* dout = (double*)malloc(sizeof(double) * (size_t)h);
+        double* dfc2 = (double*)malloc(sizeof(double) * (size_t)f);
+        double* dfc1 = (double*)malloc(sizeof(double) * (size_t)(2 * f));
+        double* ya = (double*)malloc(sizeof(double) * (size_t)h);
+        double* dxa = (double*)malloc(sizeof(double) * (size_t)h);
+        double dg[64];
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t i = 0; i < nt; ++i) {
+            const int64_t t = tokens[i];
+            for (int64_t c = 0; c < h; ++c) {
+                xt[c] = bf2d(x[t * h + c]);
+                dyt[c] = dy ? bf2d(dy[t * h + c]) : 0.0;
+                ya[c] = 0.0;
+                dxa[c] = 0.0;
+            }
+            for (int64_t j = 0; j < k; ++j) dg[j] = 0.0;
+            if (!dropped[t]) {
+                for (int64_t j = 0; j < k; ++j) {
+                    const int32_t e = experts[t * k + j];
+                    const double g = gates[t * k + j];
+                    const uint16_t* w1e = w1 + (int64_t)e * 2 * f * h;
+                    const uint16_t* w2e = w2 + (int64_t)e * h * f;
+                    for (int64_t q = 0; q < 2 * f; ++q) fc1[q] = dot_bd(xt, w1e + q * h, h);
+                    for (int64_t q = 0; q < f; ++q)
+                        fc2_in[q] = fc1[q] * silu_d(fc1[f + q]) * (gate_after ? 1.0 : g);
+                    for (int64_t c = 0; c < h; ++c) out[c] = dot_bd(fc2_in, w2e + c * f, f);
+                    for (int64_t c = 0; c < h; ++c) ya[c] += gate_after ? g * out[c] : out[c];
+                    if (!dy) continue;
+                    if (gate_after) {
+                        double s = 0.0;
+                        for (int64_t c = 0; c < h; ++c) {
+                            s += dyt[c] * out[c];
+                            dout[c] = g * dyt[c];
+                        }
+                        dg[j] += s;
+                    } else {
+                        for (int64_t c = 0; c < h; ++c) dout[c] = dyt[c];
+                    }
+                    for (int64_t q = 0; q < f; ++q) dfc2[q] = 0.0;
+                    for (int64_t c = 0; c < h; ++c) {
+                        const double d = dout[c];
+                        const uint16_t* w = w2e + c * f;
+                        for (int64_t q = 0; q < f; ++q) dfc2[q] += d * bf2d(w[q]);
+                    }
+                    const double gg = gate_after ? 1.0 : g;
+                    double sg = 0.0;
+                    for (int64_t q = 0; q < f; ++q) {
+                        const double a = fc1[q], b = fc1[f + q];
+                        sg += dfc2[q] * a * silu_d(b);
+                        dfc1[q] = dfc2[q] * gg * silu_d(b);
+                        dfc1[f + q] = dfc2[q] * gg * a * dsilu_d(b);
+                    }
+                    if (!gate_after) dg[j] += sg;
+                    for (int64_t q = 0; q < 2 * f; ++q) {
+                        const double d = dfc1[q];
+                        const uint16_t* w = w1e + q * h;
+                        for (int64_t c = 0; c < h; ++c) dxa[c] += d * bf2d(w[c]);
+                    }
+                }
+                if (dy && wr) {
+                    double sdg = 0.0;
+                    for (int64_t j = 0; j < k; ++j) sdg += gates[t * k + j] * dg[j];
+                    for (int64_t j = 0; j < k; ++j) {
+                        const double dl = gates[t * k + j] * (dg[j] - sdg);
+                        const uint16_t* w = wr + (int64_t)experts[t * k + j] * h;
+                        for (int64_t c = 0; c < h; ++c) dxa[c] += dl * bf2d(w[c]);
+                    }
+                }
+            }
+            for (int64_t c = 0; c < h; ++c) y[i * h + c] = (float)ya[c];
+            if (dy) {
+                for (int64_t c = 0; c < h; ++c) dx[i * h + c] = (float)dxa[c];
+                for (int64_t j = 0; j < k; ++j) dgates[i * k + j] = (float)dg[j];
+            }
+        }
+        free(xt); free(dyt); free(fc1); free(fc2_in); free(out); free(dout); free(dfc2);
+        free(dfc1); free(ya); free(dxa);
+    }
+    (void)E;
+}
+
+/* Sampled columns of the expert weight gradients over ALL tokens
+ * (graph.cpp:376-398 wgrad nodes). For each sampled intermediate column
+ * j = cols[c] in [0, f):
+ *   dw1_rows[e][2c]   = dW1[e][j, :]     = sum_t dfc1_a[t, j] x[t, :]
+ *   dw1_rows[e][2c+1] = dW1[e][f+j, :]   = sum_t dfc1_b[t, j] x[t, :]
+ *   dw2_cols[e][c]    = dW2[e][:, j]     = sum_t dout[t, :] fc2_in[t, j]
+ * Column j needs only x.w1[j], x.w1[f+j] and dout.w2[:, j] per row, so the
+ * cost is O(T k h) per column. Outputs: dw1_rows [E, 2nc, h], dw2_cols
+ * [E, nc, h] (fp32). Parallel over experts; rows of an expert in token order. */
+void orc_moe_wgrad_cols_bf16(const uint16_t* x, const uint16_t* dy, const int32_t* experts,
+                             const float* gates, const uint8_t* dropped, const uint16_t* w1,
+                             const uint16_t* w2, int64_t T, int64_t h, int64_t f, int64_t E,
+                             int64_t k, int gate_after, const int64_t* cols, int64_t nc,
+                             float* dw1_rows, float* dw2_cols) {
+#pragma omp parallel
+    {
+        double* xt = (double*)malloc(sizeof(double) * (size_t)h);
+        double* dout = (double*)malloc(sizeof(double) * (size_t)h);
+        double* a1 = (double*)calloc((size_t)(2 * nc * h), sizeof(double));
+        double* a2 = (double*)calloc((size_t)(nc * h), sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t e = 0; e < E; ++e) {
+            memset(a1, 0, sizeof(double) * (size_t)(2 * nc * h));
+            memset(a2, 0, sizeof(double) * (size_t)(nc * h));
+            const uint16_t* w1e = w1 + e * 2 * f * h;
+            const uint16_t* w2e = w2 + e * h * f;
+            for (int64_t t = 0; t < T; ++t) {
+                if (dropped[t]) continue;
+                for (int64_t s = 0; s < k; ++s) {
+                    if (experts[t * k + s] != e) continue;
+                    const double g = gates[t * k + s];
+                    for (int64_t c = 0; c < h; ++c) {
+                        xt[c] = bf2d(x[t * h + c]);
+                        dout[c] = (gate_after ? g : 1.0) * bf2d(dy[t * h + c]);
+                    }
+                    const double gg = gate_after ? 1.0 : g;
+                    for (int64_t ci = 0; ci < nc; ++ci) {
+                        const int64_t j = cols[ci];
+                        const double a = dot_bd(xt, w1e + j * h, h);
+                        const double b = dot_bd(xt, w1e + (f + j) * h, h);
+                        double d2 = 0.0;
+                        for (int64_t c = 0; c < h; ++c) d2 += dout[c] * bf2d(w2e[c * f + j]);
+                        const double da = d2 * gg * silu_d(b);
+                        const double db = d2 * gg * a * dsilu_d(b);
+                        const double fin = a * silu_d(b) * gg;
+                        double* r1 = a1 + (2 * ci) * h;
+                        double* r2 = a1 + (2 * ci + 1) * h;
+                        double* r3 = a2 + ci * h;
+                        for (int64_t c = 0; c < h; ++c) {
+                            r1[c] += da * xt[c];
+                            r2[c] += db * xt[c];
+                            r3[c] += fin * dout[c];
+                        }
+                    }
+                }
+            }
+            for (int64_t i = 0; i < 2 * nc * h; ++i) dw1_rows[e * 2 * nc * h + i] = (float)a1[i];
+            for (int64_t i = 0; i < nc * h; ++i) dw2_cols[e * nc * h + i] = (float)a2[i];
+        }
+        free(xt); free(dout); free(a1); free(a2);
+    }
 }

@@ -322,3 +322,75 @@ def orc_moe_backward(x, dy, experts, gates, logits, dropped, w1, w2, wr, tokens=
         C.c_int(int(gate_after)), _p(_ptr(tokens)), _i64(nt), _p(_ptr(dx)), _p(_ptr(dg)),
         nul(dw1), nul(dw2), nul(dwr))
     return dict(dx=dx, dgates=dg, dw1=dw1, dw2=dw2, dwr=dwr)
+
+
+# ----------------------------------------------------------------------------
+# full-shape sampled parity (bf16 inputs, binary64 accumulation)
+# ----------------------------------------------------------------------------
+def _u16(a):
+    """bf16 torch tensor / uint16 numpy array -> contiguous uint16 numpy."""
+    if hasattr(a, "view") and hasattr(a, "dtype") and str(a.dtype) == "torch.bfloat16":
+        import torch
+        return a.contiguous().cpu().view(torch.int16).numpy().view(np.uint16)
+    return np.ascontiguousarray(a, np.uint16)
+
+
+def orc_moe_rows_bf16(x, dy, experts, gates, dropped, w1, w2, wr, tokens, gate_after=False):
+    """y, dx, dgates of the sampled tokens. x/dy/w1/w2/wr are bf16 (torch) or
+    their uint16 bit patterns; dy or wr may be None."""
+    x, w1, w2 = _u16(x), _u16(w1), _u16(w2)
+    dy = None if dy is None else _u16(dy)
+    wr = None if wr is None else _u16(wr)
+    T, h = x.shape
+    E, f2, _ = w1.shape
+    f = f2 // 2
+    experts = np.ascontiguousarray(experts, np.int32)
+    k = experts.shape[1]
+    tokens = np.ascontiguousarray(tokens, np.int64)
+    nt = len(tokens)
+    y = np.zeros((nt, h), np.float32)
+    dx = np.zeros((nt, h), np.float32)
+    dg = np.zeros((nt, k), np.float32)
+    nul = lambda a: _p(None) if a is None else _p(_ptr(a))  # noqa: E731
+    oracle_lib().orc_moe_rows_bf16(
+        _p(_ptr(x)), nul(dy), _p(_ptr(experts)), _p(_ptr(np.ascontiguousarray(gates, np.float32))),
+        _p(_ptr(np.ascontiguousarray(dropped, np.uint8))), _p(_ptr(w1)), _p(_ptr(w2)), nul(wr),
+        _i64(h), _i64(f), _i64(E), _i64(k), C.c_int(int(gate_after)), _p(_ptr(tokens)), _i64(nt),
+        _p(_ptr(y)), _p(_ptr(dx)), _p(_ptr(dg)))
+    return dict(y=y, dx=dx, dgates=dg)
+
+
+def orc_moe_wgrad_cols_bf16(x, dy, experts, gates, dropped, w1, w2, cols, gate_after=False):
+    """Sampled intermediate columns j of dW1 (rows j and f+j) and dW2 (column j)
+    over all tokens: returns dw1 [E, nc, 2, h] and dw2 [E, nc, h] (fp32)."""
+    x, dy, w1, w2 = _u16(x), _u16(dy), _u16(w1), _u16(w2)
+    T, h = x.shape
+    E, f2, _ = w1.shape
+    f = f2 // 2
+    experts = np.ascontiguousarray(experts, np.int32)
+    k = experts.shape[1]
+    cols = np.ascontiguousarray(cols, np.int64)
+    nc = len(cols)
+    dw1 = np.zeros((E, nc, 2, h), np.float32)
+    dw2 = np.zeros((E, nc, h), np.float32)
+    oracle_lib().orc_moe_wgrad_cols_bf16(
+        _p(_ptr(x)), _p(_ptr(dy)), _p(_ptr(experts)), _p(_ptr(np.ascontiguousarray(gates, np.float32))),
+        _p(_ptr(np.ascontiguousarray(dropped, np.uint8))), _p(_ptr(w1)), _p(_ptr(w2)), _i64(T), _i64(h),
+        _i64(f), _i64(E), _i64(k), C.c_int(int(gate_after)), _p(_ptr(cols)), _i64(nc), _p(_ptr(dw1)),
+        _p(_ptr(dw2)))
+    return dw1, dw2
+
+
+def orc_router_wgrad_from_dgates(x, experts, gates, dgates, dropped, E):
+    """dW_r[E, h] = dlogits^T x with dlogits from the softmax-over-selected
+    backward (dl_e = g_e (dg_e - sum_j g_j dg_j)); x fp32 [T, h]."""
+    x = np.asarray(x, np.float64)
+    T, k = experts.shape
+    g = gates.astype(np.float64)
+    dg = dgates.astype(np.float64)
+    sdg = (g * dg).sum(1, keepdims=True)
+    dl = g * (dg - sdg)
+    dl[dropped.astype(bool)] = 0.0
+    D = np.zeros((T, E))
+    np.add.at(D, (np.repeat(np.arange(T), k), experts.reshape(-1)), dl.reshape(-1))
+    return D.T @ x

@@ -65,3 +65,7 @@ class AttnProjections:
 
     def error_flag(self) -> int:
         return int(lib().moe_attn_error_flag(self._h))
+
+    def status(self, stream=None) -> None:
+        """Synchronise and raise MoETimeout if a cross-GPU wait gave up."""
+        check(lib().moe_attn_status(self._h, stream_ptr(stream)))

@@ -35,6 +35,7 @@ struct moe_attn {
     uint32_t* ready = nullptr;
     uint32_t* epoch_dev = nullptr;
     int* err = nullptr;
+    int* counters = nullptr;  // dynamic tile schedule, one per plan
     bool ipc_ready = false, weights = false;
     GemmPlan p_qkv, p_out;
 };
@@ -86,7 +87,9 @@ extern "C" {
 moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_rank, int64_t tp_size,
                            int64_t rank, moe_attn** out) {
     MOE_CHECK_ARG(out, "null argument");
-    MOE_CHECK_ARG(tp_size >= 1 && tp_size <= 32 && rank >= 0 && rank < tp_size, "bad tp_size/rank");
+    // row destinations pack the owner as (owner << 27) into a signed int32
+    // (negative = skip), so owners 0..15 round-trip
+    MOE_CHECK_ARG(tp_size >= 1 && tp_size <= 16 && rank >= 0 && rank < tp_size, "bad tp_size/rank (tp_size <= 16)");
     MOE_CHECK_ARG(seq % (256 * tp_size) == 0, "seq must be a multiple of 256 * tp_size");
     MOE_CHECK_ARG(hidden % (256 * tp_size) == 0, "hidden must be a multiple of 256 * tp_size");
     MOE_CHECK_ARG(qkv_cols_per_rank % 64 == 0 && qkv_cols_per_rank >= 64, "qkv columns: multiple of 64");
@@ -118,9 +121,10 @@ moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_ran
     TRY(dalloc(&A->row_dst, A->s));
     TRY(dalloc(&A->rows_s, 1));
     TRY(dalloc(&A->rows_pad, 1));
-    TRY(dalloc(&A->ready, A->s / 128 + 1));
+    TRY(dalloc(&A->ready, A->s / 128 + 2));  // + the dispatch row-claim counter
     TRY(dalloc(&A->epoch_dev, 1));
     TRY(dalloc(&A->err, 1));
+    TRY(dalloc(&A->counters, 2));
     cudaMemset(A->epoch_dev, 0, 4);
     cudaMemset(A->err, 0, 4);
     const int32_t sv = (int32_t)A->s;
@@ -139,8 +143,10 @@ moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_ran
     A->p_qkv.dispatch = true;
     TRY(tmap_kmajor(&A->p_qkv.ta, A->x_all, A->s, A->h, 128));
     TRY(tmap_kmajor(&A->p_qkv.tb, A->wqkv, A->nq, A->h, 256 / A->cg));
+    A->p_qkv.counter = A->counters;
     A->p_out.cg = A->cg;
     A->p_out.epi = EPI_SCATTER;
+    A->p_out.counter = A->counters + 1;
     TRY(tmap_kmajor(&A->p_out.tb, A->wout, A->h, A->dh, 256 / A->cg));
 #undef TRY
     if (cudaDeviceSynchronize() != cudaSuccess) {
@@ -157,7 +163,7 @@ void moe_attn_destroy(moe_attn* A) {
     for (int p = 0; p < (int)A->peer.size(); ++p)
         if (p != A->rank && A->peer[p]) cudaIpcCloseMemHandle(A->peer[p]);
     void* bufs[] = {A->arena, A->tab, A->x_all, A->wqkv, A->wout, A->ident, A->row_dst, A->rows_s,
-                    A->rows_pad, A->ready, A->epoch_dev, A->err};
+                    A->rows_pad, A->ready, A->epoch_dev, A->err, A->counters};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete A;
@@ -184,7 +190,7 @@ moe_status moe_attn_ag_gemm(moe_attn* A, const uint16_t* d_x_shard, uint16_t* d_
     if (d_x_shard && d_x_shard != xs)
         MOE_CUDA_TRY(cudaMemcpyAsync(xs, d_x_shard, A->sr * A->h * 2, cudaMemcpyDeviceToDevice, s));
     MOE_TRY(attn_barrier(A, 0, s));  // every shard is in place before peers pull it
-    MOE_CUDA_TRY(cudaMemsetAsync(A->ready, 0, (A->s / 128 + 1) * 4, s));
+    MOE_CUDA_TRY(cudaMemsetAsync(A->ready, 0, (A->s / 128 + 2) * 4, s));
     GemmArgs a{};
     a.G = 1;
     a.group_rows = A->rows_s;
@@ -198,6 +204,7 @@ moe_status moe_attn_ag_gemm(moe_attn* A, const uint16_t* d_x_shard, uint16_t* d_
     a.src_bufs = reinterpret_cast<const uint16_t* const*>(A->tab);
     a.a_dst = A->x_all;
     a.ready = A->ready;
+    a.row_claim = reinterpret_cast<int*>(A->ready + A->s / 128 + 1);
     a.topk = 1;
     a.tokens_per_rank = (int)A->sr;
     a.err = A->err;
@@ -253,6 +260,11 @@ moe_status moe_attn_ipc_import(moe_attn* A, const void* h_blobs) {
     MOE_TRY(fill(A));
     A->ipc_ready = true;
     return MOE_OK;
+}
+
+moe_status moe_attn_status(moe_attn* A, moe_stream_t stream) {
+    MOE_CHECK_ARG(A, "null argument");
+    return flag_status(A->err, (cudaStream_t)stream, "moe_attn");
 }
 
 int moe_attn_error_flag(moe_attn* A) {

@@ -257,6 +257,77 @@ __device__ __forceinline__ float2 e4m3x2_to_f32x2(uint16_t v) {
     return __half22float2(hh);
 }
 
+// E4M3 code of a binary64 value with RNE + saturation at 448 and the 2^-9
+// subnormal quantum (numerics.cpp:50-68), computed in binary64 so no
+// intermediate rounding can move a value across a rounding midpoint.
+__device__ __forceinline__ uint8_t e4m3_rne_code(double q) {
+    if (q != q) return 0x7f;  // NaN
+    if (q == 0.0) return signbit(q) ? 0x80 : 0x00;
+    const double aq = fabs(q);
+    int e = ilogb(aq);
+    if (e < -6) e = -6;  // subnormal range: quantum 2^-9
+    const double quantum = ldexp(1.0, e - 3);
+    double r = rint(aq / quantum) * quantum;  // exact: division by a power of two
+    if (r > 448.0) r = 448.0;                 // saturate (numerics.cpp:63-65)
+    uint8_t code;
+    if (r < ldexp(1.0, -6)) {
+        code = (uint8_t)(int)(r / ldexp(1.0, -9));  // subnormal mantissa 0..7
+    } else {
+        const int ee = ilogb(r);
+        const int mant = (int)(r / ldexp(1.0, ee - 3)) - 8;
+        code = (uint8_t)(((ee + 7) << 3) | mant);
+    }
+    return (uint8_t)(code | (q < 0 ? 0x80 : 0));
+}
+
+// Block quantiser with the reference's arithmetic (numerics.cpp:149-156):
+// scale = absmax / 448 and code = E4M3(x / scale), both in binary64. The
+// hot kernels take a fast path — x * (1/scale rounded to fp32), two fp32
+// roundings, relative error < 2^-23 — and fall back to the binary64 division
+// when that quotient lies within 2^-16 quanta of an E4M3 rounding midpoint,
+// the only place the two can round differently (a quantum is >= 2^-20 of the
+// quotient's magnitude, so 2^-16 quanta is >= 8 fp32 ulps of margin). Codes
+// are therefore bit-identical to the reference for every fp32 / bf16 input.
+// The stored scale is the binary64 scale rounded once to fp32.
+struct E4m3Block {
+    double scale;  // binary64 scale (absmax / 448, or 1 for an all-zero block)
+    float inv;     // 1 / scale rounded to fp32
+    bool exact;    // 1 / scale overflows fp32 (absmax < ~1.3e-36): always divide
+};
+__device__ __forceinline__ E4m3Block e4m3_block(float amax) {
+    E4m3Block b;
+    b.scale = amax > 0.0f ? (double)amax / 448.0 : 1.0;
+    const double inv = 1.0 / b.scale;
+    b.exact = inv > 3.0e38;
+    b.inv = b.exact ? 0.0f : (float)inv;
+    return b;
+}
+// true when |q| (fp32) is within 2^-16 quanta of an E4M3 rounding midpoint
+__device__ __forceinline__ bool e4m3_near_midpoint(float q) {
+    const uint32_t bits = __float_as_uint(q) & 0x7fffffffu;
+    int e = (int)(bits >> 23) - 127;
+    if (e < -6) e = -6;
+    // t = |q| / quantum, quantum = 2^(e-3): exact power-of-two scaling
+    const float t = __uint_as_float(bits) * __uint_as_float((uint32_t)(127 - (e - 3)) << 23);
+    return fabsf(t - floorf(t) - 0.5f) < 1.52587890625e-5f;  // 2^-16
+}
+__device__ __forceinline__ uint8_t e4m3_code(float x, const E4m3Block& b) {
+    if (b.exact) return e4m3_rne_code((double)x / b.scale);
+    const float q = x * b.inv;
+    if (e4m3_near_midpoint(q) && fabsf(q) < 464.0f) return e4m3_rne_code((double)x / b.scale);
+    return (uint8_t)(f32x2_to_e4m3x2(q, 0.0f) & 0xff);
+}
+// two codes packed (lo = first), fast path through one cvt
+__device__ __forceinline__ uint16_t e4m3x2_code(float x0, float x1, const E4m3Block& b) {
+    if (!b.exact) {
+        const float q0 = x0 * b.inv, q1 = x1 * b.inv;
+        const bool n0 = e4m3_near_midpoint(q0) && fabsf(q0) < 464.0f;
+        const bool n1 = e4m3_near_midpoint(q1) && fabsf(q1) < 464.0f;
+        if (!(n0 | n1)) return f32x2_to_e4m3x2(q0, q1);
+    }
+    return (uint16_t)e4m3_code(x0, b) | ((uint16_t)e4m3_code(x1, b) << 8);
+}
+
 // --- system-scope flags for cross-GPU signalling ----------------------------
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

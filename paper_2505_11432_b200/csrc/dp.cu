@@ -53,12 +53,18 @@ moe_status dalloc(T** p, size_t count) {
 // (fp32 elements [c*CH, (c+1)*CH)) writes bf16 bytes [2c*CH, 2(c+1)*CH), which
 // overlap exactly the fp32 input of chunk c/2; so chunk c publishes "read" once
 // its input is in registers and writes only after chunk c/2 has published.
-// Dependencies point to strictly lower chunks, chunks are taken in increasing
-// order per CTA and the grid is co-resident (one CTA per SM), so it cannot
-// deadlock.
+// Dependencies point to strictly lower chunks and chunks are claimed in
+// increasing order from a counter (chunk_flag[nchunks]) by whichever CTA asks
+// next, so the chunk a CTA waits for is held by a CTA that is already running:
+// no deadlock whatever part of the grid is resident.
 __global__ void __launch_bounds__(kCastThreads) dp_cast_inplace_kernel(float* buf, int64_t nchunks,
                                                                         uint32_t* chunk_flag, int* err) {
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    __shared__ int64_t s_c;
+    for (;;) {
+        if (threadIdx.x == 0) s_c = (int64_t)atomicAdd(&chunk_flag[nchunks], 1u);
+        __syncthreads();
+        const int64_t c = s_c;
+        if (c >= nchunks) break;
         const float4* src = reinterpret_cast<const float4*>(buf + c * kChunk);
         uint32_t pk[kCastVec][2];
 #pragma unroll
@@ -82,6 +88,7 @@ __global__ void __launch_bounds__(kCastThreads) dp_cast_inplace_kernel(float* bu
         uint2* dst = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(buf) + c * kChunk);
 #pragma unroll
         for (int v = 0; v < kCastVec; ++v) dst[v * kCastThreads + threadIdx.x] = make_uint2(pk[v][0], pk[v][1]);
+        __syncthreads();  // s_c is reused by the next claim
     }
 }
 
@@ -205,7 +212,7 @@ moe_status moe_dp_create(int64_t count, int64_t dp_size, int64_t rank, moe_dp** 
     D->peer.assign(D->n, nullptr);
     D->peer[D->rank] = D->arena;
     TRY(dalloc(&D->tab, 2 * D->n));
-    TRY(dalloc(&D->chunk_flag, D->nchunks));
+    TRY(dalloc(&D->chunk_flag, D->nchunks + 1));  // + the chunk-claim counter
     TRY(dalloc(&D->epoch_dev, 1));
     TRY(dalloc(&D->err, 1));
     cudaMemset(D->epoch_dev, 0, 4);
@@ -252,7 +259,7 @@ moe_status moe_dp_reduce_scatter(moe_dp* D, moe_stream_t stream) {
         MOE_CUDA_TRY(cudaGetLastError());
         return MOE_OK;
     }
-    MOE_CUDA_TRY(cudaMemsetAsync(D->chunk_flag, 0, D->nchunks * 4, s));
+    MOE_CUDA_TRY(cudaMemsetAsync(D->chunk_flag, 0, (D->nchunks + 1) * 4, s));
     dp_cast_inplace_kernel<<<(unsigned)std::min<int64_t>(D->nchunks, kNumSMs * 4), kCastThreads, 0, s>>>(
         buf, D->nchunks, D->chunk_flag, D->err);
     count_launch();
@@ -304,6 +311,11 @@ moe_status moe_dp_ipc_import(moe_dp* D, const void* h_blobs) {
     MOE_TRY(fill(D));
     D->ipc_ready = true;
     return MOE_OK;
+}
+
+moe_status moe_dp_status(moe_dp* D, moe_stream_t stream) {
+    MOE_CHECK_ARG(D, "null argument");
+    return flag_status(D->err, (cudaStream_t)stream, "moe_dp");
 }
 
 int moe_dp_error_flag(moe_dp* D) {

@@ -9,9 +9,12 @@
 
 namespace moe {
 
-// Dynamic tile schedule counters: one int per launch from a per-device ring,
-// zeroed on the launch's stream just before it (graph-capturable). A slot is
-// reused only after kCounters later launches.
+// Dynamic tile schedule counters of the stateless operators (moe_grouped_gemm):
+// one int per launch from a per-device ring, zeroed on the launch's stream
+// just before it. A slot is reused only after kCounters later launches, so do
+// not keep a graph that captured moe_grouped_gemm while issuing thousands of
+// eager ones concurrently. Layer / attention / Ulysses plans own their
+// counters (GemmPlan::counter).
 static int* tile_counter_slot(int dev) {
     constexpr int kDevices = 64, kCounters = 4096;
     static int* base[kDevices] = {};
@@ -68,9 +71,13 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     static const bool static_tiles = getenv("MOE_STATIC_TILES") != nullptr;
     // (the kernel keeps the static stride for K-grouped and multi-group K >= 8192 GEMMs)
     if (!a.tile_counter && !static_tiles && !p.k_grouped && (a.K < 8192 || a.G == 1)) {
-        int dev = 0;
-        MOE_CUDA_TRY(cudaGetDevice(&dev));
-        a.tile_counter = tile_counter_slot(dev);
+        if (p.counter) {
+            a.tile_counter = p.counter;
+        } else {
+            int dev = 0;
+            MOE_CUDA_TRY(cudaGetDevice(&dev));
+            a.tile_counter = tile_counter_slot(dev);
+        }
         if (a.tile_counter) MOE_CUDA_TRY(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), s));
     }
 #define MOE_GEMM_CASE(BN, CG, AMN, BMN, KG, EPI)                                              \
@@ -185,4 +192,57 @@ extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b,
         MOE_TRY(tmap_mnmajor(&p.tb, d_b, total_rows, N));
     }
     return gemm_launch(p, a, (cudaStream_t)stream);
+}
+
+namespace {
+__global__ void identity_rows_kernel(int32_t* v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (int32_t)i;
+}
+}  // namespace
+
+/* The FP8 combine-payload epilogue (EPI_SCATTER_FP8) on its own: row r of the
+ * grouped GEMM goes to row r of d_codes / d_scales (one destination rank). */
+extern "C" moe_status moe_grouped_gemm_e4m3(const uint16_t* d_a, const uint16_t* d_b, uint8_t* d_codes,
+                                            float* d_scales, int32_t groups, const int32_t* d_group_rows,
+                                            int64_t total_rows, int64_t N, int64_t K, int32_t b_mn_major,
+                                            int32_t cta_pair, moe_stream_t stream) {
+    MOE_CHECK_ARG(d_a && d_b && d_codes && d_scales && d_group_rows, "null pointer");
+    MOE_CHECK_ARG(N % 256 == 0 && K % 64 == 0, "N must be a multiple of 256, K of 64");
+    MOE_CHECK_ARG(total_rows >= 0 && total_rows < (1ll << 27), "total_rows must be < 2^27");
+    MOE_CHECK_ARG(cta_pair == 0 || cta_pair == 1, "cta_pair must be 0 or 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    GemmPlan p;
+    p.cg = cta_pair ? 2 : 1;
+    p.b_mn = b_mn_major != 0;
+    p.epi = EPI_SCATTER_FP8;
+    MOE_TRY(tmap_kmajor(&p.ta, d_a, total_rows, K, 128));
+    GemmArgs a{};
+    a.G = groups;
+    a.group_rows = d_group_rows;
+    a.N = (int)N;
+    a.K = (int)K;
+    a.ldo = N;
+    if (!p.b_mn) {
+        a.b_group_stride = (int)N;
+        MOE_TRY(tmap_kmajor(&p.tb, d_b, (int64_t)groups * N, K, 256 / p.cg));
+    } else {
+        a.b_group_stride = (int)K;
+        MOE_TRY(tmap_mnmajor(&p.tb, d_b, (int64_t)groups * K, N));
+    }
+    // identity destinations on "rank 0" = the caller's buffers
+    void* ws = nullptr;
+    MOE_CUDA_TRY(cudaMallocAsync(&ws, 64 + (size_t)std::max<int64_t>(total_rows, 1) * 4, s));
+    void* tables[2] = {d_codes, d_scales};
+    MOE_CUDA_TRY(cudaMemcpyAsync(ws, tables, sizeof(tables), cudaMemcpyHostToDevice, s));
+    int32_t* rows = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + 64);
+    identity_rows_kernel<<<kNumSMs, 256, 0, s>>>(rows, total_rows);
+    count_launch();
+    a.row_dst = rows;
+    a.rank_base = reinterpret_cast<void* const*>(ws);
+    a.rank_scale_base = reinterpret_cast<void* const*>(ws) + 1;
+    moe_status st = gemm_launch(p, a, s);
+    cudaStreamSynchronize(s);  // the host table above must outlive the copy
+    cudaFreeAsync(ws, s);
+    return st;
 }

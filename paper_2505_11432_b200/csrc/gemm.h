@@ -14,6 +14,10 @@ struct GemmPlan {
     int epi = EPI_STORE_BF16;
     bool dispatch = false;  // fused AG + scatter of the A operand
     int grid = 0;  // 0 = one CTA per SM
+    // dynamic-schedule tile counter owned by the plan's object (layer, attn,
+    // ulysses), so a CUDA graph that captured it never shares it with a later
+    // eager launch; nullptr = the stateless operators' per-device ring
+    int* counter = nullptr;
 };
 
 moe_status gemm_launch(const GemmPlan& p, const GemmArgs& a, cudaStream_t s);

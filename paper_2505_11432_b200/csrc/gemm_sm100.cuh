@@ -74,6 +74,9 @@ struct GemmArgs {
     const uint16_t* const* src_bufs;    // per source rank: token rows [T_r, K]
     uint16_t* a_dst;                    // A operand base (permuted rows) written in-kernel
     uint32_t* ready;                    // [padded rows / TILE_M] rows landed per tile block
+    int* row_claim;                     // rows are claimed in order from this counter (zeroed
+                                        // before the launch): any resident comm warp can fill any
+                                        // row, so no CTA waits on rows owned by an unscheduled CTA
     int topk, tokens_per_rank;
     int* err;                           // set to 2 on a dispatch wait timeout
     // FP8 communication
@@ -460,13 +463,14 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
 #pragma unroll
             for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(__uint_as_float(r[i])));
         }
-        const float scale = amax > 0.0f ? amax / 448.0f : 1.0f;
-        const float inv = 1.0f / scale;
+        // binary64 scale and reference-exact codes (numerics.cpp:149-156; common.cuh)
+        const E4m3Block blk = e4m3_block(amax);
         uint8_t* codes = nullptr;
         if (dst >= 0) {
             const int64_t drow = dst & ((1 << 27) - 1);
             codes = reinterpret_cast<uint8_t*>(args.rank_base[dst >> 27]) + drow * args.ldo + n0;
-            reinterpret_cast<float*>(args.rank_scale_base[dst >> 27])[drow * (args.ldo / 128) + (n0 + c_lo) / 128] = scale;
+            reinterpret_cast<float*>(args.rank_scale_base[dst >> 27])[drow * (args.ldo / 128) + (n0 + c_lo) / 128] =
+                (float)blk.scale;
         }
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
@@ -477,8 +481,8 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             uint32_t pk[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const uint16_t lo = f32x2_to_e4m3x2(__uint_as_float(r[4 * q]) * inv, __uint_as_float(r[4 * q + 1]) * inv);
-                const uint16_t hi = f32x2_to_e4m3x2(__uint_as_float(r[4 * q + 2]) * inv, __uint_as_float(r[4 * q + 3]) * inv);
+                const uint16_t lo = e4m3x2_code(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), blk);
+                const uint16_t hi = e4m3x2_code(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), blk);
                 pk[q] = (uint32_t)lo | ((uint32_t)hi << 16);
             }
             *reinterpret_cast<uint4*>(codes + c0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -569,10 +573,22 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
 // tile block's count before loading (tile-level AG -> GEMM overlap, the
 // reference's AG+scatter+GroupedGEMM fused pair, schedule.cpp:225-242).
 template <int TILE_M>
-__device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid, int nw, int lane) {
+__device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int lane) {
     const int total = *a.nrows_pad;
     const int nvec = K / 8;
-    for (int pp = wid; pp < total; pp += nw) {
+    // Rows are claimed CLAIM at a time in increasing order by whichever comm
+    // warp asks next. Every claimed row belongs to a running warp and the only
+    // wait inside a row (dedup: row_done[ds], ds < pp) points at an earlier
+    // claim, so the rows every tile waits for always arrive, whatever subset of
+    // the grid is resident (another stream may hold SMs).
+    constexpr int CLAIM = 4;
+    for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(a.row_claim, CLAIM);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= total) break;
+    const int claim_end = min(base + CLAIM, total);
+    for (int pp = base; pp < claim_end; ++pp) {
         const int i = a.pad_row_tok[pp];
         uint4* d = reinterpret_cast<uint4*>(a.a_dst + (int64_t)pp * K);
         const int ds = (a.dup_src && i >= 0) ? a.dup_src[pp] : -1;
@@ -683,6 +699,7 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int wid,
             fence_proxy_async_global();
             red_release_gpu_add(&a.ready[pp / 128], 1u);
         }
+    }
     }
 }
 
@@ -1018,9 +1035,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
         }
     } else if (DISPATCH && warp >= 2 + Cfg::EPI_WARPS) {
         // ===================== dispatch (comm warps) =====================
-        const int cw = warp - 2 - Cfg::EPI_WARPS;
-        dispatch_warp<TILE_M>(args, args.K, (int)blockIdx.x * Cfg::COMM_WARPS + cw,
-                              (int)gridDim.x * Cfg::COMM_WARPS, lane);
+        dispatch_warp<TILE_M>(args, args.K, lane);
     } else {
         // ===================== epilogue (warps 2..9) =====================
         const int ew = warp - 2;

@@ -97,7 +97,9 @@ struct moe_layer {
     uint32_t* row_done = nullptr;
     bool fused_dispatch = true;
     int* err = nullptr;
+    int* err_host = nullptr;  // pinned mirror of *err, refreshed at the end of multi-GPU calls
     uint32_t* epoch_dev = nullptr;
+    int* counters = nullptr;  // dynamic tile schedule counters, one per GEMM plan
     bool router_attr = false;
     bool weights_set = false, routing_set = false, fwd_done = false, ipc_ready = false;
     // GEMM plans (tensor maps fixed at create)
@@ -181,15 +183,19 @@ moe_status build_plans(moe_layer* L) {
     L->p_fc1_wgrad.a_mn = L->p_fc1_wgrad.b_mn = L->p_fc1_wgrad.k_grouped = true;
     MOE_TRY(tmap_mnmajor(&L->p_fc1_wgrad.ta, L->dfc1, Mp, 2 * f));
     MOE_TRY(tmap_mnmajor(&L->p_fc1_wgrad.tb, L->x_perm, Mp, h));
+    int ci = 0;
     for (GemmPlan* p : {&L->p_fc1, &L->p_fc2, &L->p_fc2_dgrad, &L->p_fc2_wgrad, &L->p_fc1_dgrad,
-                        &L->p_fc1_wgrad})
+                        &L->p_fc1_wgrad}) {
         p->cg = L->cg;
+        p->counter = L->counters + ci++;
+    }
     // router logits[T_r, E] = x . wr^T on the tensor cores when W_r does not
     // fit in shared memory (DeepSeek shape: E = 256, h = 7168)
     L->gemm_router = (size_t)L->E * h * 4 > 200 * 1024 || L->E > 64;
     if (L->gemm_router) {
         L->p_router = GemmPlan{};
         L->p_router.epi = EPI_STORE_F32;
+        L->p_router.counter = L->counters + 6;
         // only T_r/128 x E/128 output tiles: single-CTA 128 x 128 tiles keep
         // 4x more SMs busy than 256 x 256 pairs (E = 256: 49 -> ~20 us)
         L->p_router.bn = 128;
@@ -205,6 +211,7 @@ moe_status build_plans(moe_layer* L) {
     if (L->gemm_router_wgrad) {
         L->p_router_wgrad = GemmPlan{};
         L->p_router_wgrad.epi = EPI_STORE_F32;
+        L->p_router_wgrad.counter = L->counters + 7;
         L->p_router_wgrad.cg = 2;
         L->p_router_wgrad.a_mn = L->p_router_wgrad.b_mn = L->p_router_wgrad.k_grouped = true;
         MOE_TRY(tmap_mnmajor(&L->p_router_wgrad.ta, L->dlogits_bf16, L->Tr, L->E));
@@ -224,6 +231,7 @@ void set_dispatch(moe_layer* L, GemmArgs& a, bool backward, uint16_t* dst) {
     a.nrows_pad = L->gpad_off + L->el;
     a.a_dst = dst;
     a.ready = L->ready;
+    a.row_claim = reinterpret_cast<int*>(L->ready + L->Mp / L->pad + 1);
     a.topk = (int)L->k;
     a.tokens_per_rank = (int)L->Tr;
     a.err = L->err;
@@ -261,6 +269,22 @@ moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
     return MOE_OK;
 }
 
+// A timeout of an earlier call that has reached the host (non-blocking).
+moe_status pending_timeout(moe_layer* L) {
+    const int v = *reinterpret_cast<volatile int*>(L->err_host);
+    if (v == 0) return MOE_OK;
+    return set_error(MOE_ERR_TIMEOUT, "moe_layer: an earlier call's cross-GPU wait timed out (kind %d); "
+                     "its results are invalid (moe_layer_clear_error resets)", v);
+}
+
+// Mirror the device flag into pinned host memory at the end of a multi-GPU
+// call (one 4-byte copy; graph-capturable).
+moe_status mirror_error(moe_layer* L, cudaStream_t s) {
+    if (L->n == 1 || L->comm_local) return MOE_OK;
+    MOE_CUDA_TRY(cudaMemcpyAsync(L->err_host, L->err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    return MOE_OK;
+}
+
 moe_status quantize_rows(const uint16_t* x, int64_t rows, int64_t cols, bool per_token,
                          uint8_t* codes, float* scales, cudaStream_t s) {
     const int grid = (int)std::min<int64_t>((rows + 7) / 8, kNumSMs * 8);
@@ -286,8 +310,10 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     MOE_CHECK_ARG(c.ffn_hidden % 256 == 0, "ffn_hidden must be a multiple of 256");
     MOE_CHECK_ARG(c.num_experts >= 1 && c.top_k >= 1 && c.top_k <= 8 && c.top_k <= c.num_experts,
                   "need 1 <= top_k <= min(8, num_experts)");
-    MOE_CHECK_ARG(c.ep_size >= 1 && c.ep_size <= 32 && c.num_experts % c.ep_size == 0,
-                  "num_experts must be divisible by ep_size (<= 32)");
+    // row destinations pack the source rank as (rank << 27) | row into a signed
+    // int32 (negative = padding row), so ranks 0..15 round-trip
+    MOE_CHECK_ARG(c.ep_size >= 1 && c.ep_size <= 16 && c.num_experts % c.ep_size == 0,
+                  "num_experts must be divisible by ep_size (<= 16)");
     MOE_CHECK_ARG(c.rank >= 0 && c.rank < c.ep_size, "rank out of range");
     MOE_CHECK_ARG(c.num_experts / c.ep_size <= 256, "at most 256 local experts");
     MOE_CHECK_ARG(c.comm_format == MOE_COMM_BF16 || c.comm_format == MOE_COMM_FP8,
@@ -380,7 +406,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->dfc1, Mp * 2 * f));
     TRY_ALLOC(dalloc(&L->dgate_part, Mp * (f / 256) * 2));
     TRY_ALLOC(dalloc(&L->dlogits, Tr * L->E));
-    TRY_ALLOC(dalloc(&L->ready, Mp / L->pad + 1));
+    TRY_ALLOC(dalloc(&L->ready, Mp / L->pad + 2));  // + the dispatch row-claim counter
     TRY_ALLOC(dalloc(&L->first_row, L->T));
     TRY_ALLOC(dalloc(&L->dup_src, Mp));
     TRY_ALLOC(dalloc(&L->row_done, Mp));
@@ -390,6 +416,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->tab_local, F_COUNT * L->n));
     TRY_ALLOC(dalloc(&L->err, 1));
     TRY_ALLOC(dalloc(&L->epoch_dev, 1));
+    TRY_ALLOC(dalloc(&L->counters, 8));
     TRY_ALLOC(dalloc(&L->router_rows, 1));
     L->norm = c.ffn_norm != 0;
     if (L->norm) {
@@ -402,6 +429,11 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     }
     TRY_ALLOC(dalloc(&L->dlogits_bf16, Tr * L->E));
     cudaMemset(L->err, 0, sizeof(int));
+    if (cudaHostAlloc(&L->err_host, sizeof(int), cudaHostAllocDefault) != cudaSuccess) {
+        moe_layer_destroy(L);
+        return set_error(MOE_ERR_CUDA, "pinned error flag allocation failed");
+    }
+    *L->err_host = 0;
     cudaMemset(L->epoch_dev, 0, sizeof(uint32_t));
     // the unfused (reference-structure) dispatch path is kept for A/B runs;
     // gate-after-fc2 backward needs the fused path's row scaling
@@ -441,12 +473,13 @@ void moe_layer_destroy(moe_layer* L) {
                     L->row_gate, L->x_perm, L->fc1_out, L->fc2_in, L->dy_perm, L->dfc1,
                     L->dgate_part, L->dlogits, L->rw_part, L->ready, L->first_row, L->dup_src, L->row_done,
                     L->tab_remote, L->tab_local,
-                    L->err, L->epoch_dev, L->router_rows, L->dlogits_bf16, L->x_res, L->dxn, L->gamma, L->rstd,
+                    L->err, L->epoch_dev, L->counters, L->router_rows, L->dlogits_bf16, L->x_res, L->dxn, L->gamma, L->rstd,
                     L->dgamma, L->dgamma_part};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
         if (L->ev[i]) cudaEventDestroy(L->ev[i]);
+    if (L->err_host) cudaFreeHost(L->err_host);
     delete L;
 }
 
@@ -494,6 +527,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     MOE_CHECK_ARG(L->weights_set, "weights not set");
     MOE_CHECK_ARG(L->cfg.route_mode == 0 || L->routing_set, "injected routing not set");
     MOE_CHECK_ARG(L->n == 1 || L->ipc_ready, "ep_size > 1 requires moe_layer_ipc_import");
+    MOE_TRY(pending_timeout(L));
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
     uint16_t* x_sym = L->mine<uint16_t>(F_X);
@@ -576,7 +610,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     // dispatch: AG + local scatter (rows pulled from the owning rank)
     L->mark(PH_DISPATCH, s);
     if (L->fused_dispatch) {
-        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 1) * 4, s));
+        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 2) * 4, s));
         if (L->dedup) MOE_CUDA_TRY(cudaMemsetAsync(L->row_done, 0, L->Mp * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
@@ -634,6 +668,7 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     L->mark(PH_FWD_END, s);
+    MOE_TRY(mirror_error(L, s));
     L->fwd_done = true;
     return MOE_OK;
 }
@@ -643,6 +678,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
                                  void* dx_ready_event, moe_stream_t stream) {
     MOE_CHECK_ARG(L && d_dy && d_dx, "null argument");
     MOE_CHECK_ARG(L->fwd_done, "backward needs a preceding forward");
+    MOE_TRY(pending_timeout(L));
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
     uint16_t* dy_sym = L->mine<uint16_t>(F_DY);
@@ -671,7 +707,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     MOE_TRY(barrier(L, 2, s, 1));
     // AG(dy) + scatter into permuted order (fused into the fc2 dgrad GEMM)
     if (L->fused_dispatch) {
-        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 1) * 4, s));
+        MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 2) * 4, s));
         if (L->dedup && !L->gate_after) MOE_CUDA_TRY(cudaMemsetAsync(L->row_done, 0, L->Mp * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
@@ -812,6 +848,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         }
     }
     MOE_CUDA_TRY(cudaGetLastError());
+    MOE_TRY(mirror_error(L, s));
     L->mark(PH_END, s);
     return MOE_OK;
 }
@@ -902,6 +939,28 @@ moe_status moe_layer_set_fused_dispatch(moe_layer* L, int fused) {
 moe_status moe_layer_set_comm_mode(moe_layer* L, int compute_only) {
     MOE_CHECK_ARG(L, "null argument");
     L->comm_local = compute_only != 0;
+    return MOE_OK;
+}
+
+moe_status moe_quantize_e4m3_fast(const uint16_t* d_x, int64_t rows, int64_t cols, int32_t group,
+                                  uint8_t* d_codes, float* d_scales, moe_stream_t stream) {
+    MOE_CHECK_ARG(d_x && d_codes && d_scales, "null argument");
+    MOE_CHECK_ARG(group == 0 || group == 128, "group must be 0 (per-token) or 128");
+    MOE_CHECK_ARG(rows >= 0 && cols > 0 && cols % 128 == 0, "cols must be a positive multiple of 128");
+    if (rows == 0) return MOE_OK;
+    return quantize_rows(d_x, rows, cols, group == 0, d_codes, d_scales, (cudaStream_t)stream);
+}
+
+moe_status moe_layer_status(moe_layer* L, moe_stream_t stream) {
+    MOE_CHECK_ARG(L, "null argument");
+    return flag_status(L->err, (cudaStream_t)stream, "moe_layer");
+}
+
+moe_status moe_layer_clear_error(moe_layer* L) {
+    MOE_CHECK_ARG(L, "null argument");
+    MOE_CUDA_TRY(cudaDeviceSynchronize());
+    MOE_CUDA_TRY(cudaMemset(L->err, 0, sizeof(int)));
+    *L->err_host = 0;
     return MOE_OK;
 }
 

@@ -289,7 +289,9 @@ static __global__ void dgate_after_kernel(const uint16_t* __restrict__ dy, const
 // Source-side E4M3 quantisation of this rank's rows before they are pulled
 // over NVLink (FP8 communication): GROUP = 0 -> one scale
 // per row (per_token, forward), else one per GROUP columns (grouped-128,
-// backward). fp32 arithmetic, RNE + saturation at 448.
+// backward). Codes bit-identical to the reference quantize (binary64
+// x / scale, numerics.cpp:149-156) through e4m3_block / e4m3x2_code
+// (common.cuh): fp32 fast path, binary64 division near rounding midpoints.
 template <int GROUP>
 static __global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int rows, int cols,
                                      uint8_t* __restrict__ codes, float* __restrict__ scales) {
@@ -311,9 +313,8 @@ static __global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int 
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-            const float scale = m > 0.0f ? m / 448.0f : 1.0f;
-            const float inv = 1.0f / scale;
-            if (lane == 0) scales[r] = scale;
+            const E4m3Block blk = e4m3_block(m);
+            if (lane == 0) scales[r] = (float)blk.scale;
             for (int v = lane; v < cols / 8; v += 32) {
                 const uint4 a = xr[v];
                 const uint32_t w[4] = {a.x, a.y, a.z, a.w};
@@ -321,8 +322,8 @@ static __global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int 
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     const float2 p0 = unpack_bf16x2(w[2 * q]), p1 = unpack_bf16x2(w[2 * q + 1]);
-                    pk[q] = (uint32_t)f32x2_to_e4m3x2(p0.x * inv, p0.y * inv) |
-                            ((uint32_t)f32x2_to_e4m3x2(p1.x * inv, p1.y * inv) << 16);
+                    pk[q] = (uint32_t)e4m3x2_code(p0.x, p0.y, blk) |
+                            ((uint32_t)e4m3x2_code(p1.x, p1.y, blk) << 16);
                 }
                 *reinterpret_cast<uint2*>(codes + (int64_t)r * cols + v * 8) = make_uint2(pk[0], pk[1]);
             }
@@ -342,16 +343,15 @@ static __global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int 
                 }
 #pragma unroll
                 for (int off = LPG / 2; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-                const float scale = m > 0.0f ? m / 448.0f : 1.0f;
-                const float inv = 1.0f / scale;
+                const E4m3Block blk = e4m3_block(m);
                 if (v < cols / 8) {
-                    if ((lane % LPG) == 0) scales[(int64_t)r * (cols / GROUP) + (v * 8) / GROUP] = scale;
+                    if ((lane % LPG) == 0) scales[(int64_t)r * (cols / GROUP) + (v * 8) / GROUP] = (float)blk.scale;
                     uint32_t pk[2];
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         const float2 p0 = unpack_bf16x2(w[2 * q]), p1 = unpack_bf16x2(w[2 * q + 1]);
-                        pk[q] = (uint32_t)f32x2_to_e4m3x2(p0.x * inv, p0.y * inv) |
-                                ((uint32_t)f32x2_to_e4m3x2(p1.x * inv, p1.y * inv) << 16);
+                        pk[q] = (uint32_t)e4m3x2_code(p0.x, p0.y, blk) |
+                                ((uint32_t)e4m3x2_code(p1.x, p1.y, blk) << 16);
                     }
                     *reinterpret_cast<uint2*>(codes + (int64_t)r * cols + v * 8) = make_uint2(pk[0], pk[1]);
                 }

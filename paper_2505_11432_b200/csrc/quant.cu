@@ -12,26 +12,8 @@
 
 namespace moe {
 
-__device__ __forceinline__ uint8_t e4m3_rne_code(double q) {
-    if (q != q) return 0x7f;  // NaN
-    if (q == 0.0) return signbit(q) ? 0x80 : 0x00;
-    const double aq = fabs(q);
-    int e = ilogb(aq);
-    if (e < -6) e = -6;  // subnormal range: quantum 2^-9
-    const double quantum = ldexp(1.0, e - 3);
-    double r = rint(aq / quantum) * quantum;  // exact: division by a power of two
-    if (r > 448.0) r = 448.0;                 // saturate (no inf in E4M3 training use)
-    // r is exactly representable: encode
-    uint8_t code;
-    if (r < ldexp(1.0, -6)) {
-        code = (uint8_t)(int)(r / ldexp(1.0, -9));  // subnormal mantissa 0..7
-    } else {
-        int ee = ilogb(r);
-        const int mant = (int)(r / ldexp(1.0, ee - 3)) - 8;
-        code = (uint8_t)(((ee + 7) << 3) | mant);
-    }
-    return (uint8_t)(code | (q < 0 ? 0x80 : 0));
-}
+// e4m3_rne_code (binary64 RNE + saturation) lives in common.cuh: the
+// layer's hot quantisers fall back to it near rounding midpoints.
 
 template <bool F32>
 __global__ void quantize_rows_kernel(const void* __restrict__ xv, int cols,

@@ -61,6 +61,18 @@ moe_status make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType 
     return MOE_OK;
 }
 
+moe_status flag_status(const int* d_err, cudaStream_t s, const char* what) {
+    MOE_CUDA_TRY(cudaStreamSynchronize(s));
+    int v = 0;
+    MOE_CUDA_TRY(cudaMemcpy(&v, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (v == 0) return MOE_OK;
+    static const char* kinds[] = {"", "cross-GPU flag barrier", "fused-dispatch row arrival",
+                                  "DP in-place cast chunk"};
+    return set_error(MOE_ERR_TIMEOUT, "%s: a %s wait exceeded its bound (a peer rank stalled or "
+                     "failed); results of the affected calls are invalid", what,
+                     (v >= 1 && v <= 3) ? kinds[v] : "device");
+}
+
 }  // namespace moe
 
 using namespace moe;

@@ -45,6 +45,11 @@ moe_status launch_balance_counts(const int32_t* experts, const uint8_t* dropped,
                                  int64_t E, int64_t k, int64_t n, int64_t* load,
                                  int64_t* assigned, int64_t* ndrop, cudaStream_t s);
 
+// Device error flag of a handle -> status: synchronises `s`, then returns
+// MOE_ERR_TIMEOUT when a bounded cross-GPU wait gave up (1 = flag barrier,
+// 2 = fused-dispatch row wait, 3 = DP in-place cast wait).
+moe_status flag_status(const int* d_err, cudaStream_t s, const char* what);
+
 // ---- quant.cu ----
 moe_status launch_quantize_e4m3_rows(const void* x, bool x_is_f32, int64_t rows, int64_t cols,
                                      uint8_t* codes, float* scales, cudaStream_t s);

@@ -36,6 +36,7 @@ struct moe_ulysses {
     uint32_t* ready = nullptr;
     uint32_t* epoch_dev = nullptr;
     int* err = nullptr;
+    int* counters = nullptr;  // dynamic tile schedule, one per plan
     bool ipc_ready = false, weights = false;
     GemmPlan p_qkv, p_out;
 };
@@ -113,9 +114,10 @@ moe_status moe_ulysses_create(int64_t seq, int64_t hidden, int64_t qkv_cols, int
     TRY(dalloc(&U->wout, U->h * U->h));
     TRY(dalloc(&U->ident, U->sr));
     TRY(dalloc(&U->rows_sr, 1));
-    TRY(dalloc(&U->ready, U->sr / 128 + 1));
+    TRY(dalloc(&U->ready, U->sr / 128 + 2));  // + the dispatch row-claim counter
     TRY(dalloc(&U->epoch_dev, 1));
     TRY(dalloc(&U->err, 1));
+    TRY(dalloc(&U->counters, 2));
     cudaMemset(U->epoch_dev, 0, 4);
     cudaMemset(U->err, 0, 4);
     const int32_t sv = (int32_t)U->sr;
@@ -129,11 +131,13 @@ moe_status moe_ulysses_create(int64_t seq, int64_t hidden, int64_t qkv_cols, int
     // GEMM + A2A: A = x_shard (bound per call), B = wqkv [nqkv, h]
     U->p_qkv.cg = U->cg;
     U->p_qkv.epi = EPI_STORE_BF16;
+    U->p_qkv.counter = U->counters;
     TRY(tmap_kmajor(&U->p_qkv.tb, U->wqkv, U->nqkv, U->h, 256 / U->cg));
     // A2A + GEMM: A = o_seq [sr, h] gathered in-kernel, B = wout [h, h]
     U->p_out.cg = U->cg;
     U->p_out.epi = EPI_STORE_BF16;
     U->p_out.dispatch = true;
+    U->p_out.counter = U->counters + 1;
     TRY(tmap_kmajor(&U->p_out.ta, U->o_seq, U->sr, U->h, 128));
     TRY(tmap_kmajor(&U->p_out.tb, U->wout, U->h, U->h, 256 / U->cg));
 #undef TRY
@@ -151,7 +155,7 @@ void moe_ulysses_destroy(moe_ulysses* U) {
     for (int p = 0; p < (int)U->peer.size(); ++p)
         if (p != U->rank && U->peer[p]) cudaIpcCloseMemHandle(U->peer[p]);
     void* bufs[] = {U->arena, U->tab, U->o_seq, U->wqkv, U->wout, U->ident, U->rows_sr,
-                    U->ready, U->epoch_dev, U->err};
+                    U->ready, U->epoch_dev, U->err, U->counters};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete U;
@@ -204,7 +208,7 @@ moe_status moe_ulysses_a2a_out_proj(moe_ulysses* U, const uint16_t* d_o_heads, u
     if (d_o_heads && d_o_heads != ob)
         MOE_CUDA_TRY(cudaMemcpyAsync(ob, d_o_heads, U->s * U->dh * 2, cudaMemcpyDeviceToDevice, s));
     MOE_TRY(u_barrier(U, 2, s));  // every rank's attention output is in place
-    MOE_CUDA_TRY(cudaMemsetAsync(U->ready, 0, (U->sr / 128 + 1) * 4, s));
+    MOE_CUDA_TRY(cudaMemsetAsync(U->ready, 0, (U->sr / 128 + 2) * 4, s));
     GemmArgs a{};
     a.G = 1;
     a.group_rows = U->rows_sr;
@@ -218,6 +222,7 @@ moe_status moe_ulysses_a2a_out_proj(moe_ulysses* U, const uint16_t* d_o_heads, u
     a.src_bufs = reinterpret_cast<const uint16_t* const*>(U->tab + U->n);
     a.a_dst = U->o_seq;
     a.ready = U->ready;
+    a.row_claim = reinterpret_cast<int*>(U->ready + U->sr / 128 + 1);
     a.topk = 1;
     a.tokens_per_rank = (int)U->sr;
     a.err = U->err;
@@ -252,6 +257,11 @@ moe_status moe_ulysses_ipc_import(moe_ulysses* U, const void* h_blobs) {
     MOE_TRY(fill(U));
     U->ipc_ready = true;
     return MOE_OK;
+}
+
+moe_status moe_ulysses_status(moe_ulysses* U, moe_stream_t stream) {
+    MOE_CHECK_ARG(U, "null argument");
+    return flag_status(U->err, (cudaStream_t)stream, "moe_ulysses");
 }
 
 int moe_ulysses_error_flag(moe_ulysses* U) {

@@ -61,3 +61,7 @@ class DpGradSync:
 
     def error_flag(self) -> int:
         return int(lib().moe_dp_error_flag(self._h))
+
+    def status(self, stream=None) -> None:
+        """Synchronise and raise MoETimeout if a cross-GPU wait gave up."""
+        check(lib().moe_dp_status(self._h, stream_ptr(stream)))

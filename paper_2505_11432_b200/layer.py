@@ -44,6 +44,18 @@ def _view(p, shape, dtype):
     return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
 
 
+def _check(t, shape, dtype, name):
+    """Shape / dtype / layout of a tensor handed to the C ABI as a raw pointer."""
+    if t is None:
+        return None
+    require_cuda(t)
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+        raise DomainError(f"{name} must be {dtype} {list(shape)}, got {t.dtype} {list(t.shape)}")
+    if not t.is_contiguous():
+        raise DomainError(f"{name} must be contiguous")
+    return t
+
+
 GATE_ORDERS = {"before_fc2_in": 0, "before_fc2": 0, "after_fc2_out": 1, "after_fc2": 1}
 
 
@@ -83,6 +95,8 @@ class MoELayer:
     def set_weights(self, w1: torch.Tensor, w2: torch.Tensor, wr: torch.Tensor | None = None, stream=None):
         """w1 [E_local, 2f, h] ([a | b] rows), w2 [E_local, h, f], wr [E, h]; bf16."""
         require_cuda(w1, w2, wr)
+        if w1.dtype != torch.bfloat16 or w2.dtype != torch.bfloat16 or (wr is not None and wr.dtype != torch.bfloat16):
+            raise DomainError("weights must be bf16")
         if w1.shape != (self.el, 2 * self.f, self.h) or w2.shape != (self.el, self.h, self.f):
             raise DomainError("weight shapes must be w1 [E/n, 2f, h], w2 [E/n, h, f]")
         if wr is not None and wr.shape != (self.E, self.h):
@@ -103,6 +117,8 @@ class MoELayer:
 
     def set_routing(self, experts: torch.Tensor, gates: torch.Tensor, stream=None):
         require_cuda(experts, gates)
+        if tuple(experts.shape) != (self.Tr, self.k) or tuple(gates.shape) != (self.Tr, self.k):
+            raise DomainError(f"experts / gates must be [{self.Tr}, {self.k}]")
         self._route_keep = (experts.to(torch.int32).contiguous(), gates.float().contiguous())
         check(lib().moe_layer_set_routing(self._h, ptr(self._route_keep[0]), ptr(self._route_keep[1]),
                                           stream_ptr(stream)))
@@ -110,9 +126,10 @@ class MoELayer:
     def forward(self, x: torch.Tensor | None, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         if x is not None:
             require_cuda(x)
-            x = x.contiguous()
+            x = _check(x.contiguous(), (self.Tr, self.h), torch.bfloat16, "x")
         if y is None:
             y = torch.empty(self.Tr, self.h, dtype=torch.bfloat16, device="cuda")
+        _check(y, (self.Tr, self.h), torch.bfloat16, "y")
         check(lib().moe_layer_forward(self._h, ptr(x), ptr(y), stream_ptr(stream)))
         return y
 
@@ -121,7 +138,7 @@ class MoELayer:
         """dx first (fc2 dgrad + SwiGLU bwd, fc1 dgrad + gather, combine), then
         the weight gradients; `dx_event` is recorded as soon as dx is final."""
         require_cuda(dy)
-        dy = dy.contiguous()
+        dy = _check(dy.contiguous(), (self.Tr, self.h), torch.bfloat16, "dy")
         if dx is None:
             dx = torch.empty(self.Tr, self.h, dtype=torch.bfloat16, device="cuda")
         if want_weight_grads:
@@ -131,6 +148,10 @@ class MoELayer:
                 dw2 = torch.empty(self.el, self.h, self.f, dtype=torch.bfloat16, device="cuda")
             if dwr is None:
                 dwr = torch.empty(self.E, self.h, dtype=torch.float32, device="cuda")
+        _check(dx, (self.Tr, self.h), torch.bfloat16, "dx")
+        _check(dw1, (self.el, 2 * self.f, self.h), torch.bfloat16, "dw1")
+        _check(dw2, (self.el, self.h, self.f), torch.bfloat16, "dw2")
+        _check(dwr, (self.E, self.h), torch.float32, "dwr")
         ev = C.c_void_p(dx_event.cuda_event) if dx_event is not None else C.c_void_p(None)
         check(lib().moe_layer_backward_ex(self._h, ptr(dy), ptr(dx), ptr(dw1), ptr(dw2), ptr(dwr), ev,
                                           stream_ptr(stream)))
@@ -174,6 +195,13 @@ class MoELayer:
 
     def error_flag(self) -> int:
         return int(lib().moe_layer_error_flag(self._h))
+
+    def status(self, stream=None) -> None:
+        """Synchronise and raise MoETimeout if a cross-GPU wait gave up."""
+        check(lib().moe_layer_status(self._h, stream_ptr(stream)))
+
+    def clear_error(self) -> None:
+        check(lib().moe_layer_clear_error(self._h))
 
     # ------------------------------------------------------------------
     def connect(self, group=None):

@@ -66,3 +66,33 @@ def ffn_forward_f32(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor, wr: tor
                                     int(gate_order.startswith("after")), ptr(experts), ptr(gates), ptr(y),
                                     ptr(ex), ptr(g), ptr(lg), ptr(dr), stream_ptr(stream)))
     return y, ex, g, lg, dr
+
+
+def quantize_e4m3_fast(x: torch.Tensor, group: int = 0, stream=None):
+    """The layer's dispatch-payload quantiser: bf16 [rows, cols] -> E4M3 codes
+    (uint8 bits) + fp32 scales; group 0 = per-token (scales [rows]), 128 =
+    grouped-128 (scales [rows, cols/128])."""
+    require_cuda(x)
+    if x.dtype != torch.bfloat16 or x.dim() != 2:
+        raise DomainError("quantize_e4m3_fast takes a bf16 [rows, cols] tensor")
+    rows, cols = x.shape
+    codes = torch.empty(rows, cols, dtype=torch.uint8, device=x.device)
+    scales = torch.empty((rows,) if group == 0 else (rows, cols // 128), dtype=torch.float32, device=x.device)
+    check(lib().moe_quantize_e4m3_fast(ptr(x.contiguous()), i64(rows), i64(cols), int(group), ptr(codes),
+                                       ptr(scales), stream_ptr(stream)))
+    return codes, scales
+
+
+def grouped_gemm_e4m3(a: torch.Tensor, b: torch.Tensor, group_rows: torch.Tensor, *, N: int, K: int,
+                      b_mn_major=False, cta_pair=False, stream=None):
+    """M-grouped GEMM whose epilogue quantises the fp32 accumulators
+    grouped-128 to E4M3 (the fc2 / fc1-dgrad FP8 combine payload):
+    codes [rows, N] uint8 + scales [rows, N/128] fp32."""
+    require_cuda(a, b, group_rows)
+    rows = int(a.shape[0])
+    codes = torch.empty(rows, N, dtype=torch.uint8, device=a.device)
+    scales = torch.empty(rows, N // 128, dtype=torch.float32, device=a.device)
+    check(lib().moe_grouped_gemm_e4m3(ptr(a), ptr(b), ptr(codes), ptr(scales), int(group_rows.shape[0]),
+                                      ptr(group_rows), i64(rows), i64(N), i64(K), int(bool(b_mn_major)),
+                                      int(bool(cta_pair)), stream_ptr(stream)))
+    return codes, scales

@@ -72,3 +72,7 @@ class UlyssesProjections:
 
     def error_flag(self) -> int:
         return int(lib().moe_ulysses_error_flag(self._h))
+
+    def status(self, stream=None) -> None:
+        """Synchronise and raise MoETimeout if a cross-GPU wait gave up."""
+        check(lib().moe_ulysses_status(self._h, stream_ptr(stream)))

@@ -54,3 +54,27 @@ def test_ep2_several_experts_per_token_on_a_rank(dedup):
 def test_ep4_fine_grained_dedup():
     """DeepSeek-style routing at small scale: E = 32, k = 8, EP = 4, dedup on, drops."""
     _run(4, {"MP_CF": "1.25", "MP_E": "32", "MP_K": "8", "MP_TR": "256"})
+
+
+def _run_full(n, cfg):
+    env = dict(os.environ, MP_CFG=cfg)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29641", os.path.join(ROOT, "tests", "mp_fullshape_check.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    line = [ln for ln in p.stdout.splitlines() if "MP_FULL_RESULT" in ln]
+    assert line, p.stdout[-2000:]
+    print(line[0])
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
+@pytest.mark.parametrize("cfg", ["cfg2_mixtral", "cfg3_deepseek", "cfg5_fp8_zipf"])
+def test_ep4_full_shape_parity(cfg):
+    """BASELINE configs[1], [2], [4] at EP = 4, T_r = 4096 per rank: sampled
+    fwd+bwd parity against the oracle, every rank's scatter map bit-exact."""
+    _run_full(4, cfg)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_ep2_full_shape_parity_mixtral():
+    _run_full(2, "cfg2_mixtral")

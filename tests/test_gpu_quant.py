@@ -86,3 +86,61 @@ def test_reference_test_numerics_against_gpu_adapter():
     p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     print(p.stdout[-3000:])
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+
+
+def _decode(codes_u8):
+    return torch.from_numpy(codes_u8).view(torch.float8_e4m3fn).double().numpy()
+
+
+def _stress_bf16_rows(rows, cols, seed):
+    """bf16 rows with varied magnitudes: random, all-zero, tiny (amax below
+    ~1.3e-36, where 1/scale overflows fp32), and power-of-two scales that make
+    x/scale land exactly on E4M3 rounding midpoints (RNE ties)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((rows, cols)).astype(np.float32) * 10.0 ** rng.uniform(-3, 3, (rows, 1))
+    x[1] = 0.0
+    x[2] *= 1e-38
+    ties = (rng.integers(8, 16, (8, cols)) + 0.5) * 2.0 ** rng.integers(-9, 3, (8, cols)).astype(np.float64)
+    x[3:11] = np.clip(ties * np.sign(rng.standard_normal((8, cols))), -56.0, 56.0) / 8
+    x[3:11, 0] = 56.0 / 8                     # amax = 448 * 2^-6: exact ties after scaling
+    return torch.from_numpy(x).bfloat16()
+
+
+@pytest.mark.parametrize("group", [0, 128])
+def test_layer_dispatch_quantiser_bit_exact_vs_reference(group):
+    """The quantiser the layer runs on its dispatch payloads (quantize_fast_kernel:
+    per-token forward x, grouped-128 backward dy) against the reference's own
+    quantize (oracle/_ref, numerics.cpp:113-160) on the same bf16 values."""
+    import pyoracle as P
+    from paper_2505_11432_b200 import ops
+    xb = _stress_bf16_rows(64, 4096, 3)
+    codes, scales = ops.quantize_e4m3_fast(xb.cuda(), group=group)
+    x64 = xb.float().numpy().astype(np.float64)
+    quant = P.ref_quantize if P.ref_available() else P.orc_quantize
+    want_codes, want_scales = quant(x64, "per_token" if group == 0 else "grouped", "fp8_e4m3", 128)
+    got = _decode(codes.cpu().numpy())
+    assert (got == want_codes).all(), int((got != want_codes).sum())
+    np.testing.assert_array_equal(scales.cpu().numpy().ravel(), want_scales.astype(np.float32))
+
+
+@pytest.mark.parametrize("cta_pair", [False, True])
+def test_combine_payload_epilogue_bit_exact_vs_reference(cta_pair):
+    """EPI_SCATTER_FP8 (fc2 / fc1-dgrad FP8 combine payload): the grouped-128
+    codes and scales it writes equal the reference quantize applied to the
+    fp32 accumulators of the same GEMM (EPI_STORE_F32, same tiles)."""
+    import pyoracle as P
+    from paper_2505_11432_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(5)
+    G, K, N = 3, 512, 1024
+    rows = torch.tensor([256, 384, 128], dtype=torch.int32, device="cuda")
+    R = int(rows.sum())
+    a = (torch.randn(R, K, device="cuda", generator=g) * 0.5).bfloat16()
+    b = (torch.randn(G * N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    acc = ops.grouped_gemm(a, b, rows, N=N, K=K, out_dtype=torch.float32, cta_pair=cta_pair)
+    codes, scales = ops.grouped_gemm_e4m3(a, b, rows, N=N, K=K, cta_pair=cta_pair)
+    torch.cuda.synchronize()
+    quant = P.ref_quantize if P.ref_available() else P.orc_quantize
+    want_codes, want_scales = quant(acc.cpu().numpy().astype(np.float64), "grouped", "fp8_e4m3", 128)
+    got = _decode(codes.cpu().numpy())
+    assert (got == want_codes).all(), int((got != want_codes).sum())
+    np.testing.assert_array_equal(scales.cpu().numpy().ravel(), want_scales.astype(np.float32))

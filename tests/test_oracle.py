@@ -148,3 +148,35 @@ def test_dense_oracle_self_consistency():
         wm[e, j, c] -= eps
         fd = (loss(wp) - loss(wm)) / (2 * eps)
         assert abs(fd - b["dw1"][e, j, c]) < 2e-2 * max(1.0, abs(fd))
+
+
+@pytest.mark.parametrize("gate_after", [False, True])
+def test_bf16_sampled_restatement_matches_dense_oracle(gate_after):
+    """The bf16-input sampled oracle (full-shape parity tests) agrees with the
+    fp32 dense oracle on rows, dgates and the sampled weight-gradient columns."""
+    import torch
+    T, h, f, E, k = 48, 64, 96, 4, 2
+    g = torch.Generator().manual_seed(3)
+    x = (torch.randn(T, h, generator=g) * 0.5).bfloat16()
+    dy = (torch.randn(T, h, generator=g) * 0.1).bfloat16()
+    w1 = (torch.randn(E, 2 * f, h, generator=g) / h ** 0.5).bfloat16()
+    w2 = (torch.randn(E, h, f, generator=g) / f ** 0.5).bfloat16()
+    wr = (torch.randn(E, h, generator=g) / h ** 0.5).bfloat16()
+    xf, dyf, w1f, w2f, wrf = (t.float().numpy() for t in (x, dy, w1, w2, wr))
+    lg, ex, gt = P.orc_router_topk(xf, wrf, k)
+    dr = np.zeros(T, np.uint8)
+    dr[5] = 1
+    toks = np.array([0, 3, 5, 17, 47])
+    r = P.orc_moe_rows_bf16(x, dy, ex, gt, dr, w1, w2, wr, toks, gate_after=gate_after)
+    oy = P.orc_moe_forward(xf, ex, gt, dr, w1f, w2f, tokens=toks, gate_after=gate_after)
+    ob = P.orc_moe_backward(xf, dyf, ex, gt, lg, dr, w1f, w2f, wrf, gate_after=gate_after)
+    np.testing.assert_allclose(r["y"], oy, rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(r["dx"], ob["dx"][toks], rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(r["dgates"], ob["dgates"][toks], rtol=1e-4, atol=1e-6)
+    cols = np.array([0, 7, f - 1])
+    dw1, dw2 = P.orc_moe_wgrad_cols_bf16(x, dy, ex, gt, dr, w1, w2, cols, gate_after=gate_after)
+    np.testing.assert_allclose(dw1[:, :, 0], ob["dw1"][:, cols], rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(dw1[:, :, 1], ob["dw1"][:, f + cols], rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(dw2, ob["dw2"][:, :, cols].transpose(0, 2, 1), rtol=1e-4, atol=1e-6)
+    dwr = P.orc_router_wgrad_from_dgates(xf, ex, gt, ob["dgates"], dr, E)
+    np.testing.assert_allclose(dwr, ob["dwr"], rtol=1e-4, atol=1e-6)
