@@ -241,7 +241,7 @@ def run_ours(args, cfg):
     injected = "routing_fixture" in cfg
     L = MoELayer(Tr, h, f, E, k, ep_size=n, rank=rank, capacity_factor=0.0,
                  gate_order=cfg.get("gate", "before_fc2_in"), comm_format=cfg.get("comm", "bf16"),
-                 route_mode="injected" if injected else "learned")
+                 route_mode="injected" if injected else "learned", ep_pattern=args.ep_pattern)
     L.set_weights(w1, w2, wr)
     if injected:
         # routing input data: the reference's simulate_routing output (committed fixture)
@@ -396,7 +396,8 @@ def run_ours(args, cfg):
     # memory-bound operators with the unfused dispatch (the reference's separate
     # scatter node) for their achieved HBM bandwidth
     membw = None
-    if cfg.get("comm", "bf16") == "bf16" and cfg.get("gate", "before_fc2_in") == "before_fc2_in":
+    if cfg.get("comm", "bf16") == "bf16" and cfg.get("gate", "before_fc2_in") == "before_fc2_in" \
+            and args.ep_pattern == "a2a":
         L.set_fused_dispatch(False)
         L.forward(None, y)
         L.backward(dy, dx, dw1, dw2, dwr)
@@ -496,6 +497,16 @@ def run_ours(args, cfg):
         bpe = 1 if cfg.get("comm", "bf16") == "fp8" else 2
         fwd_b = (pulled_fwd + remote_rows) * h * bpe  # dispatch x in + combine y out
         bwd_b = (pulled_bwd + remote_rows) * h * bpe  # dispatch dy in + combine dx out
+        if args.ep_pattern == "ag_rs":
+            # all-gather of every peer token row in; one pre-reduced partial per
+            # (remote token, this rank) out (sparse reduce-scatter)
+            ex_all = rt["experts"].cpu()
+            served = ((ex_all // el) == rank).any(1)
+            own = (torch.arange(ex_all.shape[0]) // Tr) == rank
+            rs_rows = int((served & ~own).sum().item())
+            fwd_b = ((n - 1) * Tr + rs_rows) * h * bpe
+            bwd_b = fwd_b
+            pulled_fwd = (n - 1) * Tr
         nvlink = {"remote_rows": remote_rows, "remote_tokens": remote_tokens, "rows_pulled": pulled_fwd,
                   "bytes_per_step": fwd_b + bwd_b,
                   "link_GBps_if_spread_over_step": (fwd_b + bwd_b) / (ms / 1000.0) / 1e9,
@@ -557,7 +568,7 @@ def run_ours(args, cfg):
             "config": {"workload": cfg["workload"], "hidden": h, "ffn_hidden": f, "num_experts": E,
                        "top_k": k, "tokens_per_rank": Tr, "global_tokens": Tr * n,
                        "parallelism": f"ep{n}", "comm_format": cfg.get("comm", "bf16"),
-                       "gate_order": cfg.get("gate", "before_fc2_in"),
+                       "gate_order": cfg.get("gate", "before_fc2_in"), "ep_pattern": args.ep_pattern,
                        "l2": "inputs larger than L2 (expert weights >= 2.8 GB/layer)"},
             "roofline": roof,
             "phases_ms": {kk: round(v, 4) for kk, v in phases.items()},
@@ -921,6 +932,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     ap.add_argument("--no-nccl-baseline", action="store_true")
+    ap.add_argument("--ep-pattern", default="a2a", choices=["a2a", "ag_rs"],
+                    help="EP dispatch/combine pattern (commcost.hpp:81): needed-row pulls + per-slot pushes, "
+                         "or all-gather + local scatter and per-rank pre-reduced reduce-scatter")
     ap.add_argument("--trace", default=None, help="write the measured per-phase timeline (reference trace schema)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -171,7 +171,7 @@ typedef struct moe_layer moe_layer; /* opaque */
 
 typedef enum { MOE_GATE_BEFORE_FC2 = 0, MOE_GATE_AFTER_FC2 = 1 } moe_gate_order; /* numerics.hpp:86 */
 typedef enum { MOE_COMM_BF16 = 0, MOE_COMM_FP8 = 1 } moe_comm_format;           /* config.hpp:41 */
-typedef enum { MOE_EP_AG_RS = 0, MOE_EP_A2A = 1 } moe_ep_pattern;               /* commcost.hpp:81 */
+typedef enum { MOE_EP_A2A = 0, MOE_EP_AG_RS = 1 } moe_ep_pattern;               /* commcost.hpp:81 (same order) */
 
 typedef struct {
     int64_t tokens_per_rank; /* T_r (b*s/n, graph.cpp:111-113) */

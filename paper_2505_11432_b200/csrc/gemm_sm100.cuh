@@ -97,6 +97,15 @@ struct GemmArgs {
     // already-landed row dup_src[pp] (< pp) locally instead of pulling it again
     const int32_t* dup_src;     // [padded rows] earlier row of the same token, -1 = pull
     uint32_t* row_done;         // [padded rows] set once a row has landed
+    // ep_pattern = ag_rs (commcost.hpp:81; graph.cpp:276-286 "ag_ffn_in" then
+    // "scatter"): the comm warps first all-gather every peer's token rows into
+    // the local ag_dst [n*T_r, K] (ag_rows = (n-1)*T_r claim items, peers in
+    // rotation from self_rank+1), publishing ag_ready[src][64-token chunk];
+    // the local scatter then reads peers' rows from ag_dst once their chunk
+    // has landed and this rank's own rows from src_bufs[self_rank].
+    int ag_rows, self_rank;
+    uint16_t* ag_dst;
+    uint32_t* ag_ready;
     // dynamic tile schedule: zeroed before the launch; the leader CTA's producer
     // takes tiles in order with an atomic and hands them to every role through a
     // shared-memory queue (nullptr = static stride schedule)
@@ -582,13 +591,38 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int lane
     // claim, so the rows every tile waits for always arrive, whatever subset of
     // the grid is resident (another stream may hold SMs).
     constexpr int CLAIM = 4;
+    const int nag = a.ag_rows;   // all-gather items come first in the claim order
+    const int Tr = a.tokens_per_rank;
     for (;;) {
     int base = 0;
     if (lane == 0) base = atomicAdd(a.row_claim, CLAIM);
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= total) break;
-    const int claim_end = min(base + CLAIM, total);
-    for (int pp = base; pp < claim_end; ++pp) {
+    if (base >= nag + total) break;
+    if (base < nag) {
+        // ---- AG: peer rows -> local ag_dst (NVLink pulls), rank rotation ----
+        const int q_end = min(base + CLAIM, nag);
+        for (int q = base; q < q_end; ++q) {
+            const int pi = q / Tr, tl = q - pi * Tr;
+            const int src = (a.self_rank + 1 + pi) % a.n_src;
+            const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs[src] + (int64_t)tl * K);
+            uint4* dp = reinterpret_cast<uint4*>(a.ag_dst + ((int64_t)src * Tr + tl) * K);
+            constexpr int U = 16;
+            for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+                uint4 r[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (v0 + 32 * u < nvec) r[u] = __ldcg(sp + v0 + 32 * u);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (v0 + 32 * u < nvec) dp[v0 + 32 * u] = r[u];
+            }
+            __syncwarp();
+            if (lane == 0) red_release_gpu_add(&a.ag_ready[src * ((Tr + 63) / 64) + tl / 64], 1u);
+        }
+        continue;
+    }
+    const int claim_end = min(base + CLAIM, nag + total) - nag;
+    for (int pp = base - nag; pp < claim_end; ++pp) {
         const int i = a.pad_row_tok[pp];
         uint4* d = reinterpret_cast<uint4*>(a.a_dst + (int64_t)pp * K);
         const int ds = (a.dup_src && i >= 0) ? a.dup_src[pp] : -1;
@@ -662,7 +696,25 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int lane
             } else {
                 const int t = i / a.topk;
                 const int src = t / a.tokens_per_rank;
-                sp = reinterpret_cast<const uint4*>(a.src_bufs[src] + (int64_t)(t - src * a.tokens_per_rank) * K);
+                const int tl = t - src * a.tokens_per_rank;
+                if (nag > 0 && src != a.self_rank) {
+                    // ag_rs: the row was all-gathered into ag_dst by this kernel's comm warps
+                    if (lane == 0) {
+                        const uint32_t want = (uint32_t)min(64, Tr - (tl / 64) * 64);
+                        const uint32_t* flag = &a.ag_ready[src * ((Tr + 63) / 64) + tl / 64];
+                        const uint64_t t0 = globaltimer();
+                        while (ld_acquire_gpu(flag) < want) {
+                            if (globaltimer() - t0 > 4000000000ull) {
+                                atomicExch(a.err, 2);
+                                break;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    sp = reinterpret_cast<const uint4*>(a.ag_dst + (int64_t)t * K);
+                } else {
+                    sp = reinterpret_cast<const uint4*>(a.src_bufs[src] + (int64_t)tl * K);
+                }
                 if (a.row_scale) rs = a.row_scale[pp];
             }
             for (int sg = 0; sg < nseg; ++sg) {

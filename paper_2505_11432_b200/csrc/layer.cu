@@ -31,7 +31,9 @@ size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
 // fields of the symmetric arena (same offsets on every rank)
 enum Field {
     F_X, F_DY, F_STAGE, F_DSTAGE, F_EX, F_GT, F_DGATE, F_FLAGS,
-    F_X8, F_XSC, F_DY8, F_DYSC, F_STAGE8, F_SSC, F_DSTAGE8, F_DSSC, F_COUNT
+    F_X8, F_XSC, F_DY8, F_DYSC, F_STAGE8, F_SSC, F_DSTAGE8, F_DSSC,
+    F_RSTAGE,  // ag_rs: reduce-scatter staging [T_r, n, h] (one partial per serving rank)
+    F_COUNT
 };
 }  // namespace
 
@@ -96,6 +98,15 @@ struct moe_layer {
     int32_t *first_row = nullptr, *dup_src = nullptr;
     uint32_t* row_done = nullptr;
     bool fused_dispatch = true;
+    // ep_pattern = ag_rs (n > 1): in-kernel all-gather of every peer's rows into
+    // x_all, local scatter from it; expert outputs stored locally, pre-reduced
+    // per (token, rank) and reduce-scattered to the owner
+    bool ag = false;
+    uint16_t* x_all = nullptr;      // [T, h] (x in forward, dy in backward)
+    uint32_t* ag_ready = nullptr;   // [n][ceil(T_r/64)] rows landed per 64-token chunk
+    int32_t* inv = nullptr;         // [T*k] padded row of (t, slot), -1 = not here
+    uint16_t* rows_out = nullptr;   // [Mp, h] local fc2 / fc1-dgrad output rows
+    moe::GemmPlan p_fc2_local, p_fc1_dgrad_local;
     int* err = nullptr;
     int* err_host = nullptr;  // pinned mirror of *err, refreshed at the end of multi-GPU calls
     uint32_t* epoch_dev = nullptr;
@@ -189,6 +200,13 @@ moe_status build_plans(moe_layer* L) {
         p->cg = L->cg;
         p->counter = L->counters + ci++;
     }
+    // ag_rs: the same GEMMs with a plain local row-major store epilogue
+    L->p_fc2_local = L->p_fc2;
+    L->p_fc2_local.epi = EPI_STORE_BF16;
+    L->p_fc2_local.counter = L->counters + 8;
+    L->p_fc1_dgrad_local = L->p_fc1_dgrad;
+    L->p_fc1_dgrad_local.epi = EPI_STORE_BF16;
+    L->p_fc1_dgrad_local.counter = L->counters + 9;
     // router logits[T_r, E] = x . wr^T on the tensor cores when W_r does not
     // fit in shared memory (DeepSeek shape: E = 256, h = 7168)
     L->gemm_router = (size_t)L->E * h * 4 > 200 * 1024 || L->E > 64;
@@ -235,6 +253,13 @@ void set_dispatch(moe_layer* L, GemmArgs& a, bool backward, uint16_t* dst) {
     a.topk = (int)L->k;
     a.tokens_per_rank = (int)L->Tr;
     a.err = L->err;
+    if (L->ag) {
+        a.ag_rows = (int)((L->n - 1) * L->Tr);
+        a.self_rank = (int)L->rank;
+        a.ag_dst = L->x_all;
+        a.ag_ready = L->ag_ready;
+        a.n_src = (int)L->n;
+    }
     // the backward copy would carry the first row's gate (gate after fc2): pull instead
     if (L->dedup && !(backward && L->gate_after)) {
         a.dup_src = L->dup_src;
@@ -264,6 +289,17 @@ moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
     if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
     flag_barrier_kernel<<<1, 64, 0, s>>>(L->tab<uint32_t>(F_FLAGS), slot, (int)L->n, (int)L->rank,
                                         L->epoch_dev, bump, 20ull * 1000 * 1000 * 1000, L->err);
+    count_launch();
+    MOE_CUDA_TRY(cudaGetLastError());
+    return MOE_OK;
+}
+
+// ag_rs gather + reduce-scatter: per (token, this rank) partial of the local
+// slot rows -> the owning rank's F_RSTAGE[t_local][rank].
+moe_status launch_gather_rs(moe_layer* L, cudaStream_t s) {
+    gather_rs_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->mine<int32_t>(F_EX), L->dropped, L->inv, (int)L->T, (int)L->k,
+                                                 (int)L->first, (int)L->el, (int)L->Tr, (int)L->n, (int)L->rank,
+                                                 (int)L->h, L->rows_out, L->tab<uint16_t>(F_RSTAGE));
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;
@@ -320,10 +356,17 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
                   "comm_format must be bf16 or fp8");
     MOE_CHECK_ARG(c.gate_order == MOE_GATE_BEFORE_FC2 || c.gate_order == MOE_GATE_AFTER_FC2,
                   "gate_order must be before_fc2_in or after_fc2_out");
+    MOE_CHECK_ARG(c.ep_pattern == MOE_EP_A2A || c.ep_pattern == MOE_EP_AG_RS, "ep_pattern must be a2a or ag_rs");
+    if (c.ep_pattern == MOE_EP_AG_RS && c.ep_size > 1 &&
+        (c.comm_format != MOE_COMM_BF16 || c.gate_order != MOE_GATE_BEFORE_FC2))
+        return set_error(MOE_ERR_UNSUPPORTED,
+                         "ep_pattern ag_rs is built for bf16 communication with the gate before fc2 "
+                         "(the FP8 / gate-after-fc2 path uses a2a)");
     auto* L = new moe_layer();
     L->cfg = c;
     L->fp8 = c.comm_format == MOE_COMM_FP8;
     L->gate_after = c.gate_order == MOE_GATE_AFTER_FC2;
+    L->ag = c.ep_pattern == MOE_EP_AG_RS && c.ep_size > 1;
     L->Tr = c.tokens_per_rank;
     L->n = c.ep_size;
     L->rank = c.rank;
@@ -366,6 +409,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     sizes[F_SSC] = L->fp8 ? Tr * k * (h / 128) * 4 : 0;
     sizes[F_DSTAGE8] = L->fp8 ? Tr * k * h : 0;
     sizes[F_DSSC] = L->fp8 ? Tr * k * (h / 128) * 4 : 0;
+    sizes[F_RSTAGE] = L->ag ? Tr * L->n * h * 2 : 0;
     size_t total = 0;
     for (int fld = 0; fld < F_COUNT; ++fld) {
         L->off[fld] = total;
@@ -416,7 +460,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->tab_local, F_COUNT * L->n));
     TRY_ALLOC(dalloc(&L->err, 1));
     TRY_ALLOC(dalloc(&L->epoch_dev, 1));
-    TRY_ALLOC(dalloc(&L->counters, 8));
+    TRY_ALLOC(dalloc(&L->counters, 10));
     TRY_ALLOC(dalloc(&L->router_rows, 1));
     L->norm = c.ffn_norm != 0;
     if (L->norm) {
@@ -428,6 +472,12 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
         TRY_ALLOC(dalloc(&L->dgamma_part, ((Tr + kRwChunk - 1) / kRwChunk) * h));
     }
     TRY_ALLOC(dalloc(&L->dlogits_bf16, Tr * L->E));
+    if (L->ag) {
+        TRY_ALLOC(dalloc(&L->x_all, L->T * h));
+        TRY_ALLOC(dalloc(&L->ag_ready, L->n * ((Tr + 63) / 64)));
+        TRY_ALLOC(dalloc(&L->inv, L->T * k));
+        TRY_ALLOC(dalloc(&L->rows_out, Mp * h));
+    }
     cudaMemset(L->err, 0, sizeof(int));
     if (cudaHostAlloc(&L->err_host, sizeof(int), cudaHostAllocDefault) != cudaSuccess) {
         moe_layer_destroy(L);
@@ -437,10 +487,10 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     cudaMemset(L->epoch_dev, 0, sizeof(uint32_t));
     // the unfused (reference-structure) dispatch path is kept for A/B runs;
     // gate-after-fc2 backward needs the fused path's row scaling
-    L->fused_dispatch = getenv("MOE_UNFUSED_DISPATCH") == nullptr || L->gate_after || L->fp8;
+    L->fused_dispatch = getenv("MOE_UNFUSED_DISPATCH") == nullptr || L->gate_after || L->fp8 || L->ag;
     // on by default (DeepSeek shape, EP = 4: 9.17 -> 8.93 ms per step with the
     // dynamic tile schedule; Mixtral EP = 4 unchanged); MOE_NO_DISPATCH_DEDUP=1 off
-    L->dedup = L->n > 1 && L->k > 1 && L->el > 1 && getenv("MOE_NO_DISPATCH_DEDUP") == nullptr;
+    L->dedup = L->n > 1 && L->k > 1 && L->el > 1 && !L->ag && getenv("MOE_NO_DISPATCH_DEDUP") == nullptr;
     // zero the permuted buffers once so never-written rows are finite
     cudaMemset(L->x_perm, 0, Mp * h * 2);
     cudaMemset(L->dy_perm, 0, Mp * h * 2);
@@ -474,7 +524,7 @@ void moe_layer_destroy(moe_layer* L) {
                     L->dgate_part, L->dlogits, L->rw_part, L->ready, L->first_row, L->dup_src, L->row_done,
                     L->tab_remote, L->tab_local,
                     L->err, L->epoch_dev, L->counters, L->router_rows, L->dlogits_bf16, L->x_res, L->dxn, L->gamma, L->rstd,
-                    L->dgamma, L->dgamma_part};
+                    L->dgamma, L->dgamma_part, L->x_all, L->ag_ready, L->inv, L->rows_out};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
@@ -607,10 +657,16 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         dup_src_kernel<<<kNumSMs * 2, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, L->first_row, L->dup_src);
         count_launch(2);
     }
+    if (L->ag) {
+        MOE_CUDA_TRY(cudaMemsetAsync(L->inv, 0xff, L->T * k * 4, s));
+        inverse_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, L->inv);
+        count_launch();
+    }
     // dispatch: AG + local scatter (rows pulled from the owning rank)
     L->mark(PH_DISPATCH, s);
     if (L->fused_dispatch) {
         MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 2) * 4, s));
+        if (L->ag) MOE_CUDA_TRY(cudaMemsetAsync(L->ag_ready, 0, L->n * ((Tr + 63) / 64) * 4, s));
         if (L->dedup) MOE_CUDA_TRY(cudaMemsetAsync(L->row_done, 0, L->Mp * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
@@ -647,17 +703,28 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         a.K = (int)f;
         a.b_group_stride = (int)h;
         a.ldo = h;
-        a.row_dst = L->row_dst;
-        a.rank_base = L->fp8 ? L->tab<void>(F_STAGE8) : L->tab<void>(F_STAGE);
-        a.rank_scale_base = L->tab<void>(F_SSC);
-        MOE_TRY(gemm_launch(L->p_fc2, a, s));
+        if (L->ag) {
+            // ag_rs: rows stay local; gather + reduce-scatter below
+            a.out = L->rows_out;
+            MOE_TRY(gemm_launch(L->p_fc2_local, a, s));
+        } else {
+            a.row_dst = L->row_dst;
+            a.rank_base = L->fp8 ? L->tab<void>(F_STAGE8) : L->tab<void>(F_STAGE);
+            a.rank_scale_base = L->tab<void>(F_SSC);
+            MOE_TRY(gemm_launch(L->p_fc2, a, s));
+        }
     }
+    if (L->ag) MOE_TRY(launch_gather_rs(L, s));
     MOE_TRY(barrier(L, 1, s, 0));
     // combine: fixed-order fp32 reduce over the k slots (gate after fc2 applied here)
     L->mark(PH_COMBINE, s);
     const uint8_t* drop_loc = L->dropped + L->rank * Tr;
     const float* slot_gate = L->gate_after ? L->gt_loc : nullptr;
-    if (L->fp8)
+    if (L->ag)
+        combine_rs_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->mine<uint16_t>(F_RSTAGE), L->ex_loc, drop_loc, (int)Tr,
+                                                      (int)k, (int)el, (int)L->n, (int)h, d_y, nullptr, nullptr,
+                                                      nullptr, nullptr, 0);
+    else if (L->fp8)
         launch_combine<true>(s, 
             L->mine<uint8_t>(F_STAGE8), L->mine<float>(F_SSC), drop_loc, (int)Tr, (int)k, (int)h, d_y,
             slot_gate, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
@@ -708,6 +775,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     // AG(dy) + scatter into permuted order (fused into the fc2 dgrad GEMM)
     if (L->fused_dispatch) {
         MOE_CUDA_TRY(cudaMemsetAsync(L->ready, 0, (L->Mp / L->pad + 2) * 4, s));
+        if (L->ag) MOE_CUDA_TRY(cudaMemsetAsync(L->ag_ready, 0, L->n * ((Tr + 63) / 64) * 4, s));
         if (L->dedup && !L->gate_after) MOE_CUDA_TRY(cudaMemsetAsync(L->row_done, 0, L->Mp * 4, s));
     } else {
         dispatch_rows_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->pad_tok, L->gpad_off + el, (int)k, (int)Tr,
@@ -746,11 +814,17 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.K = (int)(2 * f);
         a.b_group_stride = (int)(2 * f);
         a.ldo = h;
-        a.row_dst = L->row_dst;
-        a.rank_base = L->fp8 ? L->tab<void>(F_DSTAGE8) : L->tab<void>(F_DSTAGE);
-        a.rank_scale_base = L->tab<void>(F_DSSC);
-        MOE_TRY(gemm_launch(L->p_fc1_dgrad, a, s));
+        if (L->ag) {
+            a.out = L->rows_out;
+            MOE_TRY(gemm_launch(L->p_fc1_dgrad_local, a, s));
+        } else {
+            a.row_dst = L->row_dst;
+            a.rank_base = L->fp8 ? L->tab<void>(F_DSTAGE8) : L->tab<void>(F_DSTAGE);
+            a.rank_scale_base = L->tab<void>(F_DSSC);
+            MOE_TRY(gemm_launch(L->p_fc1_dgrad, a, s));
+        }
     }
+    if (L->ag) MOE_TRY(launch_gather_rs(L, s));
     L->mark(PH_DGATE, s);
     if (!L->gate_after) {
         dgate_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(L->dgate_part, (int)(f / 256) * 2, L->row_dst,
@@ -761,7 +835,12 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
     L->mark(PH_COMBINE_DX, s);
     const bool router = L->cfg.route_mode == 0;
     uint16_t* dx_moe = L->norm ? L->dxn : d_dx;  // gradient w.r.t. the (normalised) layer input
-    if (L->fp8)
+    if (L->ag)
+        combine_rs_kernel<<<kNumSMs * 4, 256, 0, s>>>(
+            L->mine<uint16_t>(F_RSTAGE), L->ex_loc, drop_loc, (int)Tr, (int)k, (int)el, (int)L->n, (int)h, dx_moe,
+            router ? L->gt_loc : nullptr, router ? dgate_sym : nullptr, router ? L->wr : nullptr,
+            router ? L->dlogits : nullptr, (int)L->E);
+    else if (L->fp8)
         launch_combine<true>(s, 
             L->mine<uint8_t>(F_DSTAGE8), L->mine<float>(F_DSSC), drop_loc, (int)Tr, (int)k, (int)h,
             dx_moe, nullptr, router ? L->ex_loc : nullptr, router ? L->gt_loc : nullptr,
@@ -930,8 +1009,8 @@ moe_status moe_layer_ipc_import(moe_layer* L, const void* h_blobs) {
 
 moe_status moe_layer_set_fused_dispatch(moe_layer* L, int fused) {
     MOE_CHECK_ARG(L, "null argument");
-    MOE_CHECK_ARG(fused || (!L->fp8 && !L->gate_after),
-                  "the unfused dispatch path supports bf16 comm with gate before fc2 only");
+    MOE_CHECK_ARG(fused || (!L->fp8 && !L->gate_after && !L->ag),
+                  "the unfused dispatch path supports bf16 comm, gate before fc2, ep_pattern a2a only");
     L->fused_dispatch = fused != 0;
     return MOE_OK;
 }

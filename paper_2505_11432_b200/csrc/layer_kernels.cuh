@@ -360,6 +360,148 @@ static __global__ void quantize_fast_kernel(const uint16_t* __restrict__ x, int 
     }
 }
 
+// ---------------------------------------------------------------------------
+// ep_pattern = ag_rs (commcost.hpp:81): "gather" then "rs_ffn_out"
+// (graph.cpp:302-309). The expert GEMM writes its output rows locally; each
+// rank then sums, per token, the rows of the slots it served (fixed slot
+// order, fp32) and sends ONE partial row per (token, rank) to the owner's
+// staging [T_r, n, h]; the owner adds the partials of the ranks that served
+// the token in rank order (a2a_fp32 reduction semantics over ranks,
+// numerics.cpp:172-192). Only (token, rank) pairs with a served slot move:
+// a sparse reduce-scatter, <= min(k, n) rows per token instead of k.
+// ---------------------------------------------------------------------------
+
+// inverse of the padded row map: inv[t*k + slot] = padded row (or -1)
+static __global__ void inverse_rows_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad,
+                                           int32_t* __restrict__ inv) {
+    const int total = *nrows_pad;
+    for (int pp = blockIdx.x * blockDim.x + threadIdx.x; pp < total; pp += gridDim.x * blockDim.x) {
+        const int i = pad_row_tok[pp];
+        if (i >= 0) inv[i] = pp;
+    }
+}
+
+// one warp per global token: partial = sum of this rank's slot rows -> owner
+static __global__ void gather_rs_kernel(const int32_t* __restrict__ experts, const uint8_t* __restrict__ dropped,
+                                        const int32_t* __restrict__ inv, int T, int k, int first, int el,
+                                        int tokens_per_rank, int n, int self, int h,
+                                        const uint16_t* __restrict__ rows, uint16_t* const* __restrict__ dst) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int nv16 = h / 16;
+    for (int t = warp; t < T; t += nwarps) {
+        if (dropped[t]) continue;
+        int rr[8];
+        int nr = 0;
+        for (int j = 0; j < k; ++j) {
+            const int e = experts[(int64_t)t * k + j] - first;
+            if (e >= 0 && e < el) rr[nr++] = inv[(int64_t)t * k + j];
+        }
+        if (nr == 0) continue;
+        const int src = t / tokens_per_rank;
+        uint4* o = reinterpret_cast<uint4*>(dst[src] + ((int64_t)(t - src * tokens_per_rank) * n + self) * h);
+        for (int v = lane; v < nv16; v += 32) {
+            float acc[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] = 0.0f;
+            for (int j = 0; j < nr; ++j) {
+                const uint4* sp = reinterpret_cast<const uint4*>(rows + (int64_t)rr[j] * h);
+                const uint4 s0 = sp[2 * v], s1 = sp[2 * v + 1];
+                const uint32_t w[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float2 p = unpack_bf16x2(w[q]);
+                    acc[2 * q] += p.x;
+                    acc[2 * q + 1] += p.y;
+                }
+            }
+            o[2 * v] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                                  pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+            o[2 * v + 1] = make_uint4(pack_bf16x2(acc[8], acc[9]), pack_bf16x2(acc[10], acc[11]),
+                                      pack_bf16x2(acc[12], acc[13]), pack_bf16x2(acc[14], acc[15]));
+        }
+    }
+}
+
+// owner side: y[t] = sum over the ranks that served t (rank order, fp32) of
+// the staged partials; optional router term as in combine_reduce_kernel.
+static __global__ void combine_rs_kernel(const uint16_t* __restrict__ stage, const int32_t* __restrict__ experts_loc,
+                                         const uint8_t* __restrict__ dropped, int T, int k, int el, int n, int h,
+                                         uint16_t* __restrict__ out, const float* __restrict__ gates,
+                                         const float* __restrict__ dgates, const uint16_t* __restrict__ wr,
+                                         float* __restrict__ dlogits, int E) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int nv16 = h / 16;
+    for (int t = warp; t < T; t += nwarps) {
+        uint4* o = reinterpret_cast<uint4*>(out + (int64_t)t * h);
+        if (dropped[t]) {
+            for (int v = lane; v < h / 8; v += 32) o[v] = make_uint4(0, 0, 0, 0);
+            if (dlogits) for (int e = lane; e < E; e += 32) dlogits[(int64_t)t * E + e] = 0.0f;
+            continue;
+        }
+        uint32_t mask = 0;
+        int ex[8];
+        float dl[8];
+        for (int j = 0; j < k; ++j) {
+            ex[j] = experts_loc[(int64_t)t * k + j];
+            mask |= 1u << (ex[j] / el);
+        }
+        const bool router = wr != nullptr;
+        if (router) {
+            float g[8], dg[8];
+            for (int j = 0; j < k; ++j) {
+                g[j] = gates[(int64_t)t * k + j];
+                dg[j] = dgates[(int64_t)t * k + j];
+            }
+            softmax_topk_bwd(g, dg, k, dl);
+            if (dlogits) {
+                for (int e = lane; e < E; e += 32) {
+                    float v = 0.0f;
+                    for (int j = 0; j < k; ++j) v = (ex[j] == e) ? dl[j] : v;
+                    dlogits[(int64_t)t * E + e] = v;
+                }
+            }
+        }
+        for (int v = lane; v < nv16; v += 32) {
+            float acc[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] = 0.0f;
+            for (int r = 0; r < n; ++r) {
+                if (!(mask >> r & 1u)) continue;
+                const uint4* sp = reinterpret_cast<const uint4*>(stage + ((int64_t)t * n + r) * h);
+                const uint4 s0 = sp[2 * v], s1 = sp[2 * v + 1];
+                const uint32_t w[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float2 p = unpack_bf16x2(w[q]);
+                    acc[2 * q] += p.x;
+                    acc[2 * q + 1] += p.y;
+                }
+            }
+            if (router) {
+                for (int j = 0; j < k; ++j) {
+                    const uint4* wp = reinterpret_cast<const uint4*>(wr + (int64_t)ex[j] * h);
+                    const uint4 w0 = wp[2 * v], w1 = wp[2 * v + 1];
+                    const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float2 p = unpack_bf16x2(w[q]);
+                        acc[2 * q] += dl[j] * p.x;
+                        acc[2 * q + 1] += dl[j] * p.y;
+                    }
+                }
+            }
+            o[2 * v] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                                  pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+            o[2 * v + 1] = make_uint4(pack_bf16x2(acc[8], acc[9]), pack_bf16x2(acc[10], acc[11]),
+                                      pack_bf16x2(acc[12], acc[13]), pack_bf16x2(acc[14], acc[15]));
+        }
+    }
+}
+
 // dgate of each permuted row = sum over f-tiles of the epilogue partials
 // (fixed order, deterministic), scattered to (source rank, t_local*k+slot).
 static __global__ void dgate_reduce_kernel(const float* __restrict__ part, int n_parts,

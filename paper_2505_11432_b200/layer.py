@@ -56,6 +56,7 @@ def _check(t, shape, dtype, name):
     return t
 
 
+EP_PATTERNS = {"a2a": 0, "ag_rs": 1}   # commcost.hpp:81 EpPattern order
 GATE_ORDERS = {"before_fc2_in": 0, "before_fc2": 0, "after_fc2_out": 1, "after_fc2": 1}
 
 
@@ -63,10 +64,16 @@ class MoELayer:
     def __init__(self, tokens_per_rank: int, hidden: int, ffn_hidden: int, num_experts: int,
                  top_k: int, ep_size: int = 1, rank: int = 0, capacity_factor: float = 0.0,
                  gate_order: str = "before_fc2_in", comm_format: str = "bf16",
-                 route_mode: str = "learned", ffn_norm: bool = False, norm_eps: float = 1e-6):
+                 route_mode: str = "learned", ffn_norm: bool = False, norm_eps: float = 1e-6,
+                 ep_pattern: str = "a2a"):
+        """ep_pattern (commcost.hpp:81): "a2a" = pull only the rows this rank's
+        experts need + push every (token, slot) output row to its owner;
+        "ag_rs" = all-gather every token row, local scatter, and one
+        pre-reduced partial row per (token, serving rank) reduce-scattered to
+        the owner (bf16 communication, gate before fc2)."""
         cfg = _Cfg(tokens_per_rank, hidden, ffn_hidden, num_experts, top_k, ep_size, rank,
                    float(capacity_factor), GATE_ORDERS[gate_order],
-                   {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}[comm_format], 0,
+                   {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}[comm_format], EP_PATTERNS[ep_pattern],
                    {"learned": 0, "injected": 1}[route_mode], int(bool(ffn_norm)), float(norm_eps))
         self.norm = bool(ffn_norm)
         self.cfg = cfg

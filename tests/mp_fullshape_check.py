@@ -40,7 +40,7 @@ def main():
     w1, w2, wr, x, dy = make_inputs(c, T)
     L = MoELayer(Tr, h, f, E, k, ep_size=n, rank=rank,
                  route_mode="injected" if c["route"] == "zipf" else "learned",
-                 gate_order=c["gate"], comm_format=c["comm"])
+                 gate_order=c["gate"], comm_format=c["comm"], ep_pattern=os.environ.get("MP_EP", "a2a"))
     L.set_weights(w1[rank * el:(rank + 1) * el].contiguous(), w2[rank * el:(rank + 1) * el].contiguous(), wr)
     L.connect()
     if c["route"] == "zipf":

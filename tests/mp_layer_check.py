@@ -48,7 +48,7 @@ def main():
     comm = os.environ.get("MP_COMM", "bf16")
     tol = 5e-2 if comm == "fp8" else 1e-2
     L = MoELayer(Tr, h, f, E, k, ep_size=n, rank=rank, capacity_factor=cf, gate_order=gate_order,
-                 comm_format=comm)
+                 comm_format=comm, ep_pattern=os.environ.get("MP_EP", "a2a"))
     L.set_weights(w1[rank * el:(rank + 1) * el].cuda(), w2[rank * el:(rank + 1) * el].cuda(), wr.cuda())
     L.connect()
     xs = x[rank * Tr:(rank + 1) * Tr].cuda()

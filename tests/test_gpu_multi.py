@@ -78,3 +78,26 @@ def test_ep4_full_shape_parity(cfg):
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_ep2_full_shape_parity_mixtral():
     _run_full(2, "cfg2_mixtral")
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("E,k,cf", [(8, 2, "0"), (8, 4, "1.25"), (32, 8, "0")])
+def test_ep2_ag_rs_pattern(E, k, cf):
+    """ep_pattern = ag_rs: in-kernel all-gather + local scatter, local expert
+    rows pre-reduced per (token, rank) and reduce-scattered to the owner."""
+    _run(2, {"MP_CF": cf, "MP_E": str(E), "MP_K": str(k), "MP_TR": "256", "MP_EP": "ag_rs"})
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
+def test_ep4_ag_rs_pattern():
+    _run(4, {"MP_CF": "1.25", "MP_E": "32", "MP_K": "8", "MP_TR": "256", "MP_EP": "ag_rs"})
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
+def test_ep4_full_shape_parity_deepseek_ag_rs():
+    env = dict(os.environ, MP_CFG="cfg3_deepseek", MP_EP="ag_rs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr=127.0.0.1", "--master-port=29642", os.path.join(ROOT, "tests", "mp_fullshape_check.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "MP_FULL_RESULT" in p.stdout
