@@ -132,61 +132,93 @@ class ClockSampler:
 _CPU_STATE = {}
 
 
-def cpu_reference_step(cfg, sample_tokens, seed=0, with_dense=True):
-    """One step of the reference CPU path on a bounded sample: the
-    reference's own routing maps (oracle/_ref) + the fp32 oracle's dense
-    fwd+bwd for `sample_tokens` tokens. Returns (seconds, kind, threads)."""
+def _cpu_weights(E, f, h):
+    """fp32 expert + router weights for the CPU baseline (generated once, not
+    timed). Values only set the timing, so a 64 MB N(0,1) block is tiled."""
+    key = (E, f, h)
+    if key not in _CPU_STATE:
+        _CPU_STATE.clear()
+        rng = np.random.default_rng(0)
+        blk = rng.standard_normal(1 << 24, dtype=np.float32)
+
+        def fill(shape, scale):
+            a = np.empty(shape, np.float32)
+            flat = a.reshape(-1)
+            for o in range(0, flat.size, blk.size):
+                m = min(blk.size, flat.size - o)
+                np.multiply(blk[:m], np.float32(scale), out=flat[o:o + m])
+            return a
+        w1 = fill((E, 2 * f, h), h ** -0.5)
+        w2 = fill((E, h, f), f ** -0.5)
+        wr = fill((E, h), h ** -0.5)
+        grads = (np.empty_like(w1), np.empty_like(w2), np.empty((E, h), np.float32))
+        _CPU_STATE[key] = (w1, w2, wr, grads)
+    return _CPU_STATE[key]
+
+
+def cpu_reference_step(cfg, n_ranks, max_dense_tokens=4096, seed=0):
+    """One step of the reference CPU path for the whole job (T = n_ranks x T_r
+    tokens): the reference's own routing code (oracle/_ref, single-threaded as
+    shipped: build_scatter_map + sort_tokens_for_tiles for every rank,
+    balance_metrics) on all T tokens, and the dense layer (router, fc1, SwiGLU,
+    fc2, combine, full backward incl. weight gradients) as fp32 numpy/OpenBLAS
+    on all host cores for min(T, max_dense_tokens) tokens. Returns a dict; the
+    step time is t_route + t_dense * T / S (S = T at N = 1: no extrapolation)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as P
-    h, f, E, k = cfg["hidden"], cfg["ffn_hidden"], cfg["num_experts"], cfg["top_k"]
-    S = sample_tokens
-    key = (h, f, E, k, S)
-    if key not in _CPU_STATE:  # weights generated once (not timed)
-        rng = np.random.default_rng(0)
-        w1 = rng.standard_normal((E, 2 * f, h), dtype=np.float32)
-        w1 *= np.float32(1.0 / np.sqrt(h))
-        w2 = rng.standard_normal((E, h, f), dtype=np.float32)
-        w2 *= np.float32(1.0 / np.sqrt(f))
-        wr = (rng.standard_normal((E, h), dtype=np.float32) / np.float32(np.sqrt(h)))
-        _CPU_STATE.clear()
-        _CPU_STATE[key] = (w1, w2, wr)
-    w1, w2, wr = _CPU_STATE[key]
+    from threadpoolctl import threadpool_limits
+    h, f, E, k, Tr = cfg["hidden"], cfg["ffn_hidden"], cfg["num_experts"], cfg["top_k"], cfg["tokens_per_rank"]
+    T = n_ranks * Tr
+    S = min(T, max_dense_tokens)
+    w1, w2, wr, grads = _cpu_weights(E, f, h)
     rng = np.random.default_rng(seed)
-    x = (rng.standard_normal((S, h), dtype=np.float32) * np.float32(0.5))
-    dy = (rng.standard_normal((S, h), dtype=np.float32) * np.float32(0.1))
+    x = rng.standard_normal((S, h), dtype=np.float32) * np.float32(0.5)
+    dy = rng.standard_normal((S, h), dtype=np.float32) * np.float32(0.1)
+    cores = os.cpu_count() or 1
     kind = "reference" if P.ref_available() else "port"
-    # all host cores (torchrun exports OMP_NUM_THREADS=1 to every rank)
-    P.oracle_lib().orc_set_threads(os.cpu_count() or 1)
-    threads = int(P.oracle_lib().orc_get_threads())
-    t0 = time.perf_counter()
-    logits, ex, gates = P.orc_router_topk(x, wr, k)
-    src = np.zeros(S, np.int32)
-    dr = np.zeros(S, np.uint8)
+    # routing input for all T tokens (simulate_routing = the reference's input generator, not timed)
     if kind == "reference":
-        m = P.ref_build_scatter_map(ex, src, dr, E, 1, 0)
-        P.ref_sort_tokens_for_tiles(ex, src, dr, E, 1, 0, 128)
+        ex, src, dr = P.ref_simulate_routing(T, E, k, "random", 11 + seed, n_groups=n_ranks)
+        t_route = float(np.sum(P.ref_time_routing(ex, src, dr, E, n_ranks, 128, 1))) / 1000.0
     else:
-        m = P.orc_build_scatter_map(ex, src, dr, E, 1, 0)
-        P.orc_sort_tokens_for_tiles(m["out_expert"], m["out_source_rank"], 128)
-    if with_dense:
-        P.orc_moe_forward(x, ex, gates, dr, w1, w2)
-        P.orc_moe_backward(x, dy, ex, gates, logits, dr, w1, w2, wr)
-    dt = time.perf_counter() - t0
-    return dt, kind, threads
+        ex = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+        src = (np.arange(T) // Tr).astype(np.int32)
+        dr = np.zeros(T, np.uint8)
+        t0 = time.perf_counter()
+        for r in range(n_ranks):
+            P.orc_build_scatter_map(ex, src, dr, E, n_ranks, r)
+        t_route = time.perf_counter() - t0
+    with threadpool_limits(limits=cores):
+        t0 = time.perf_counter()
+        P.np_moe_fwd_bwd(x, dy, wr, w1, w2, k, out=grads)
+        t_dense = time.perf_counter() - t0
+    t_step = t_route + t_dense * T / S
+    return dict(t_step=t_step, t_route=t_route, t_dense=t_dense, T=T, S=S, kind=kind, cores=cores,
+                value=T / t_step)
+
+
+def _cpu_sample_text(r):
+    ext = "" if r["S"] == r["T"] else f", dense time scaled x{r['T'] / r['S']:.0f} from {r['S']} tokens"
+    return (f"whole job per step: {r['T']} tokens; reference routing maps for every rank + tile layout + "
+            f"balance (oracle/_ref, 1 thread, {1000 * r['t_route']:.1f} ms) + fp32 numpy/OpenBLAS dense "
+            f"router+FFN fwd+bwd incl. weight grads on {r['cores']} threads ({r['t_dense']:.2f} s{ext})")
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    S = args.cpu_sample
+    n = args.gpus
     times = []
+    last = None
     for i in range(args.warmup + args.steps):
-        dt, kind, cores = cpu_reference_step(cfg, S, seed=i)
+        # warm-up steps run the same code on a small dense sample (pages, BLAS threads)
+        r = cpu_reference_step(cfg, n, max_dense_tokens=(256 if i < args.warmup else 4096), seed=i)
         if i >= args.warmup:
-            times.append(dt)
+            times.append(r["t_step"])
+            last = r
     ms = 1000.0 * float(np.mean(times))
-    val = S / (ms / 1000.0)
+    val = n * cfg["tokens_per_rank"] / (ms / 1000.0)
     line = {
         "impl": "reference", "metric": "moe_layer_fwd_bwd_tokens_per_s", "value": val,
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -194,10 +226,10 @@ def run_reference(args, cfg):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["workload"], "hidden": cfg["hidden"], "ffn_hidden": cfg["ffn_hidden"],
                    "num_experts": cfg["num_experts"], "top_k": cfg["top_k"],
-                   "tokens_per_rank": cfg["tokens_per_rank"], "sample_tokens_per_step": S},
-        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": kind,
-                         "sample": f"{S} tokens/step: reference routing maps (oracle/_ref) + fp32 "
-                                   f"oracle router+FFN fwd+bwd incl. weight grads, OpenMP {cores} threads"},
+                   "tokens_per_rank": cfg["tokens_per_rank"], "global_tokens": n * cfg["tokens_per_rank"],
+                   "dense_tokens_per_step": last["S"]},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": last["cores"], "kind": last["kind"],
+                         "sample": _cpu_sample_text(last)},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -320,27 +352,44 @@ def run_ours(args, cfg):
     # ---- exposed communication: T_layer - T_compute_only (schedule.cpp:149-152) ----
     exposed = None
     if world > 1:
-        # alternate normal / compute-only windows (3 each) and compare medians so
-        # that clock drift between windows does not masquerade as communication
-        def window(compute_only):
+        # exposed = T_layer - T_compute_only (schedule.cpp:149-152). Both modes run
+        # as captured CUDA graphs of the same kernels (compute-only: peer buffers
+        # replaced by local ones, no barriers); 10 alternating windows so clock
+        # drift shows up as spread instead of masquerading as communication.
+        def capture(compute_only):
             L.set_compute_only(compute_only)
             for _ in range(2):
                 step()
             sync_all()
+            if args.no_graph:
+                return step
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                step()
+            gr.replay()
+            sync_all()
+            return gr.replay
+        run_co = capture(True)
+        run_norm = capture(False)
+        wsteps = max(5, args.steps // 2)
+
+        def window(fn):
+            sync_all()
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(stream)
-            for _ in range(args.steps):
-                step()
+            for _ in range(wsteps):
+                fn()
             c1.record(stream)
             sync_all()
-            tc = torch.tensor([c0.elapsed_time(c1) / args.steps], device="cuda")
+            tc = torch.tensor([c0.elapsed_time(c1) / wsteps], device="cuda")
             dist.all_reduce(tc, op=dist.ReduceOp.MAX)
             return float(tc.item())
         t_norm, t_comp = [], []
-        for _ in range(3):
-            t_norm.append(window(False))
-            t_comp.append(window(True))
+        for _ in range(10):
+            t_norm.append(window(run_norm))
+            t_comp.append(window(run_co))
         # per-phase times in compute-only mode (where the step goes without NVLink)
+        L.set_compute_only(True)
         L.enable_timing(True)
         L.forward(None, y)
         L.backward(dy, dx, dw1, dw2, dwr)
@@ -351,12 +400,48 @@ def run_ours(args, cfg):
             step()
         sync_all()
         tn, tcm = float(np.median(t_norm)), float(np.median(t_comp))
+        diffs = np.array(t_norm) - np.array(t_comp)
         exposed = {"t_layer_ms": tn, "t_compute_only_ms": tcm,
                    "exposed_ms": tn - tcm, "exposed_pct": 100.0 * (tn - tcm) / tn,
-                   "windows_layer_ms": t_norm, "windows_compute_only_ms": t_comp,
+                   "pair_diff_ms": {"median": float(np.median(diffs)), "min": float(diffs.min()),
+                                    "max": float(diffs.max()), "p25": float(np.percentile(diffs, 25)),
+                                    "p75": float(np.percentile(diffs, 75))},
+                   "windows_layer_ms": t_norm, "windows_compute_only_ms": t_comp, "steps_per_window": wsteps,
                    "phases_compute_only_ms": {kk: round(v, 4) for kk, v in phases_co.items()},
-                   "definition": "median T_layer - median T_compute_only over 3 alternating windows (same "
-                                 "kernels, peer buffers replaced by local ones, no barriers), max over ranks"}
+                   "definition": "median T_layer - median T_compute_only over 10 alternating windows of "
+                                 "graph-replayed steps (same kernels and tile order, peer buffers replaced by "
+                                 "local ones, no barriers), max over ranks"}
+
+    # ---- %globaltimer trace of graph-replayed steps (all ranks on one clock) ----
+    gtrace = None
+    if not args.no_graph:
+        L.enable_stamps(True)
+        step()
+        sync_all()
+        gst = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gst):
+            step()
+        steps_st = []
+        for _ in range(10):
+            gst.replay()
+            sync_all()
+            ph_ns, bars = L.read_stamps()
+            steps_st.append((ph_ns, bars))
+        L.enable_stamps(False)
+        del gst
+        for _ in range(2):
+            step()
+        sync_all()
+        mine = {"rank": rank, "steps": [{"phases": p_, "barriers": {str(k_): v_ for k_, v_ in b_.items()}}
+                                        for p_, b_ in steps_st]}
+        if world > 1:
+            allst = [None] * world
+            dist.all_gather_object(allst, mine)
+        else:
+            allst = [mine]
+        if rank == 0:
+            from paper_2505_11432_b200.trace import stamp_summary
+            gtrace = stamp_summary(allst)
 
     # ---- NCCL all-to-all + cuBLAS baseline (standard unfused EP), same shapes ----
     nccl_ms = None
@@ -512,6 +597,16 @@ def run_ours(args, cfg):
                   "link_GBps_if_spread_over_step": (fwd_b + bwd_b) / (ms / 1000.0) / 1e9,
                   "link_time_ms_at_770GBps": (fwd_b + bwd_b) / 770e9 * 1000.0,
                   "note": "bytes per direction per rank; overlapped inside fc1/fc2/fc2-dgrad/fc1-dgrad"}
+    # ---- the six expert GEMMs vs torch._grouped_mm / per-expert cuBLAS, same shapes ----
+    gemm_cmp = None
+    if n == 1 and not args.no_gemm_compare and cfg.get("comm", "bf16") == "bf16":
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from cublas_gemm_baseline import compare_gemms
+        gemm_cmp = compare_gemms(h, f, [int(c) for c in cnt])
+        fused = {"fc1": "fc1", "fc2": "fc2", "fc2_dgrad": "fc2_dgrad", "fc1_dgrad": "fc1_dgrad",
+                 "fc2_wgrad": "fc2_wgrad", "fc1_wgrad": "fc1_wgrad"}
+        gemm_cmp["layer_fused_ms"] = {kk: round(phases.get(v, float("nan")), 4) for kk, v in fused.items()}
+        torch.cuda.empty_cache()
     pad = layer_pad(L)
     routing_info = {"local_rows": int(sum(cnt)), "padded_rows": int(sum((c + pad - 1) // pad * pad for c in cnt)),
                     "row_padding": pad,
@@ -575,7 +670,9 @@ def run_ours(args, cfg):
             "routing_rank0": routing_info,
             "memory_bound_ops": membw,
             "exposed_comm": exposed,
+            "graph_trace": None if gtrace is None else gtrace["summary"],
             "nvlink": nvlink,
+            "gemm_vs_cublas": gemm_cmp,
             "nvlink_dispatch_pull": nvlink_pull if membw is not None else None,
             "nccl_a2a_cublas_baseline": None if nccl_ms is None else {
                 "ms_per_step": nccl_ms, "tokens_per_s": n * Tr / (nccl_ms / 1000.0),
@@ -591,17 +688,27 @@ def run_ours(args, cfg):
         }
         if n == 1 and not args.no_cpu_baseline:
             try:
-                dt, kind, cores = cpu_reference_step(cfg, args.cpu_sample)
-                line["cpu_baseline"] = {
-                    "value": args.cpu_sample / dt, "unit": "tokens/s", "cores": cores, "kind": kind,
-                    "sample": f"{args.cpu_sample} tokens: reference routing maps + fp32 oracle "
-                              f"router+FFN fwd+bwd incl. weight grads ({cores} OpenMP threads)"}
+                r = cpu_reference_step(cfg, 1, max_dense_tokens=256)  # warm (pages, BLAS threads)
+                r = cpu_reference_step(cfg, 1)
+                line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": r["cores"],
+                                        "kind": r["kind"], "sample": _cpu_sample_text(r)}
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+            if not args.no_integer_compare:
+                try:
+                    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+                    from integer_path_bench import compare as integer_compare
+                    line["reference_integer_path"] = integer_compare()
+                except Exception as e:  # noqa: BLE001
+                    line["reference_integer_path"] = {"error": str(e)[:200]}
         if args.trace:
-            from paper_2505_11432_b200.trace import write_trace
-            write_trace(args.trace, phases, Tr * k, h, f,
-                        exposed["exposed_ms"] / 1000.0 if exposed else None)
+            from paper_2505_11432_b200.trace import write_stamp_trace, write_trace
+            if gtrace is not None:
+                write_stamp_trace(args.trace, gtrace, Tr * k, h, f,
+                                  exposed["exposed_ms"] / 1000.0 if exposed else None)
+            else:
+                write_trace(args.trace, phases, Tr * k, h, f,
+                            exposed["exposed_ms"] / 1000.0 if exposed else None)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -928,10 +1035,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-sample", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of one CUDA graph per step")
     ap.add_argument("--no-nccl-baseline", action="store_true")
+    ap.add_argument("--no-integer-compare", action="store_true",
+                    help="skip the full-shape reference integer path vs device kernels block (N=1)")
+    ap.add_argument("--no-gemm-compare", action="store_true",
+                    help="skip the per-GEMM torch._grouped_mm / cuBLAS comparison (N=1)")
     ap.add_argument("--ep-pattern", default="a2a", choices=["a2a", "ag_rs"],
                     help="EP dispatch/combine pattern (commcost.hpp:81): needed-row pulls + per-slot pushes, "
                          "or all-gather + local scatter and per-rank pre-reduced reduce-scatter")

@@ -270,6 +270,19 @@ moe_status moe_layer_phase_times(moe_layer* L, float* h_ms, int max_phases, int*
  * not meaningful in that mode; 0 restores normal operation. */
 moe_status moe_layer_set_comm_mode(moe_layer* L, int compute_only);
 
+/* %globaltimer trace of (graph-replayed) steps: with stamps enabled, every
+ * phase boundary of forward / backward records the device global timer
+ * (one 1-thread kernel per boundary, captured into graphs like the rest), and
+ * every cross-GPU flag barrier records its entry and release times (the wait
+ * for the slowest rank = rank-imbalance idle). moe_layer_read_stamps
+ * synchronises the device and copies the last step's stamps: h_ns[0..n_phases)
+ * per phase (names as moe_layer_phase_times; 0 = not reached), then
+ * h_ns[n_phases + 2*slot + {0, 1}] = barrier slot entry / release
+ * (slots 0 metadata, 1 combine, 2 dy dispatch, 3 dx combine). */
+moe_status moe_layer_enable_stamps(moe_layer* L, int enable);
+moe_status moe_layer_read_stamps(moe_layer* L, uint64_t* h_ns, int max_slots, int* n_phases,
+                                 const char** names);
+
 /* 1 (default): dispatch (AG + local scatter) fused into the fc1 / fc2-dgrad
  * GEMMs; 0: a separate memory-bound scatter kernel (the reference's unfused
  * operator structure, graph.cpp:276-286; used to measure it). */

@@ -297,7 +297,9 @@ def orc_moe_forward(x, experts, gates, dropped, w1, w2, tokens=None, gate_after=
 
 
 def orc_moe_backward(x, dy, experts, gates, logits, dropped, w1, w2, wr, tokens=None,
-                     gate_after=False, weight_grads=True):
+                     gate_after=False, weight_grads=True, out=None):
+    """out: optional preallocated (dw1, dw2, dwr) fp32 buffers, zeroed here and
+    accumulated into (saves the per-call allocation of weight-sized arrays)."""
     x = np.ascontiguousarray(x, np.float32)
     T, h = x.shape
     E, f2, _ = w1.shape
@@ -307,9 +309,14 @@ def orc_moe_backward(x, dy, experts, gates, logits, dropped, w1, w2, wr, tokens=
     nt = len(tokens)
     dx = np.zeros((nt, h), np.float32)
     dg = np.zeros((nt, k), np.float32)
-    dw1 = np.zeros_like(w1, dtype=np.float32) if weight_grads else None
-    dw2 = np.zeros_like(w2, dtype=np.float32) if weight_grads else None
-    dwr = np.zeros((E, h), np.float32) if weight_grads else None
+    if weight_grads and out is not None:
+        dw1, dw2, dwr = out
+        for a in out:
+            a.fill(0.0)
+    else:
+        dw1 = np.zeros_like(w1, dtype=np.float32) if weight_grads else None
+        dw2 = np.zeros_like(w2, dtype=np.float32) if weight_grads else None
+        dwr = np.zeros((E, h), np.float32) if weight_grads else None
     nul = lambda a: _p(None) if a is None else _p(_ptr(a))  # noqa: E731
     oracle_lib().orc_moe_backward(
         _p(_ptr(x)), _p(_ptr(np.ascontiguousarray(dy, np.float32))),
@@ -394,3 +401,96 @@ def orc_router_wgrad_from_dgates(x, experts, gates, dgates, dropped, E):
     D = np.zeros((T, E))
     np.add.at(D, (np.repeat(np.arange(T), k), experts.reshape(-1)), dl.reshape(-1))
     return D.T @ x
+
+
+def ref_time_routing(experts, src, dropped, E, n, tile_rows=128, reps=3):
+    """Reference build_scatter_map x n, sort_tokens_for_tiles x n and
+    balance_metrics timed inside the reference library (value types built once
+    outside the timed region); returns the three medians in ms."""
+    experts = np.ascontiguousarray(experts, np.int32)
+    T, k = experts.shape
+    ms = np.zeros(3)
+    st = ref_lib().ref_time_routing(_i64(T), _i64(E), _i64(k), _i64(n), _p(_ptr(experts)),
+                                    _p(_ptr(np.ascontiguousarray(src, np.int32))),
+                                    _p(_ptr(np.ascontiguousarray(dropped, np.uint8))), _i64(n), _i64(tile_rows),
+                                    C.c_int(reps), _p(_ptr(ms)))
+    if st != 0:
+        raise ValueError(f"ref_time_routing failed ({st})")
+    return ms
+
+
+def ref_time_numerics(x, vectors, gran="per_token", fmt="fp8_e4m3", group_size=128, kind="a2a_fp32"):
+    """Reference quantize and emulate_reduce timed inside the library (ms)."""
+    x = np.ascontiguousarray(x, np.float64)
+    v = np.ascontiguousarray(vectors, np.float64)
+    ms = np.zeros(2)
+    st = ref_lib().ref_time_numerics(_p(_ptr(x)), _i64(x.shape[0]), _i64(x.shape[1]), C.c_int(GRANS[gran]),
+                                     _i64(group_size), C.c_int(FORMATS[fmt]), _p(_ptr(v)), _i64(v.shape[0]),
+                                     _i64(v.shape[1]), C.c_int(0 if kind == "ring_bf16" else 1), _p(_ptr(ms)))
+    if st != 0:
+        raise ValueError(f"ref_time_numerics failed ({st})")
+    return ms
+
+
+# ----------------------------------------------------------------------------
+# fp32 numpy/BLAS restatement of the dense layer (CPU baseline at full shape)
+# ----------------------------------------------------------------------------
+def np_router_topk(x, wr, k):
+    """logits = x wr^T; top-k (ties -> lower expert id); softmax over the k."""
+    logits = x @ wr.T
+    ex = np.argsort(-logits, axis=1, kind="stable")[:, :k].astype(np.int32)
+    sel = np.take_along_axis(logits, ex, 1).astype(np.float64)
+    g = np.exp(sel - sel[:, :1])
+    g /= g.sum(1, keepdims=True)
+    return logits, ex, g.astype(np.float32)
+
+
+def np_moe_fwd_bwd(x, dy, wr, w1, w2, k, experts=None, gates=None, dropped=None, out=None):
+    """The same math as orc_moe_forward / orc_moe_backward (graph.cpp:288-296
+    forward, :333-401 backward; SwiGLU a*silu(b), gate before fc2, softmax
+    router backward), batched per expert with fp32 BLAS GEMMs. Returns y, dx,
+    dgates, (dw1, dw2, dwr); `out` = optional preallocated (dw1, dw2, dwr)."""
+    T, h = x.shape
+    E, f2, _ = w1.shape
+    f = f2 // 2
+    if experts is None:
+        logits, experts, gates = np_router_topk(x, wr, k)
+    dropped = np.zeros(T, bool) if dropped is None else dropped.astype(bool)
+    y = np.zeros((T, h), np.float32)
+    dx = np.zeros((T, h), np.float32)
+    dg = np.zeros((T, k), np.float32)
+    if out is None:
+        out = (np.empty_like(w1), np.empty_like(w2), np.empty((E, h), np.float32))
+    dw1, dw2, dwr = out
+    flat_e = experts.reshape(-1)
+    keep = ~np.repeat(dropped, k)
+    for e in range(E):
+        idx = np.nonzero((flat_e == e) & keep)[0]
+        if idx.size == 0:
+            dw1[e] = 0.0
+            dw2[e] = 0.0
+            continue
+        t_idx, s_idx = idx // k, idx % k
+        g = gates[t_idx, s_idx][:, None]
+        xe = x[t_idx]
+        h1 = xe @ w1[e].T
+        a, b = h1[:, :f], h1[:, f:]
+        sb = 1.0 / (1.0 + np.exp(-b))
+        silu = b * sb
+        z = a * silu * g
+        y[t_idx] += z @ w2[e].T
+        dout = dy[t_idx]
+        dz = dout @ w2[e]
+        dw2[e] = dout.T @ z
+        dg[t_idx, s_idx] = (dz * a * silu).sum(1)
+        dh1 = np.concatenate([dz * g * silu, dz * g * a * (sb * (1.0 + b * (1.0 - sb)))], 1)
+        dw1[e] = dh1.T @ xe
+        dx[t_idx] += dh1 @ w1[e]
+    sdg = (gates * dg).sum(1, keepdims=True)
+    dl = gates * (dg - sdg)
+    dl[dropped] = 0.0
+    dlog = np.zeros((T, E), np.float32)
+    np.put_along_axis(dlog, experts.astype(np.int64), dl, 1)
+    dx += dlog @ wr
+    dwr[...] = dlog.T @ x
+    return y, dx, dg, (dw1, dw2, dwr)

@@ -5,6 +5,8 @@
 // TEST INFRASTRUCTURE ONLY: used to pin the oracle restatement
 // (moe_oracle.c), to generate tests/golden/ fixtures, and as the
 // `--impl reference` CPU arm of bench.py. The product never links it.
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -165,6 +167,68 @@ int ref_emulate_reduce(const double* vectors, int64_t ranks, int64_t dim, int ki
         for (int64_t r = 0; r < ranks; ++r) v[r].assign(vectors + r * dim, vectors + (r + 1) * dim);
         const auto o = numerics::emulate_reduce(v, static_cast<numerics::ReduceKind>(kind));
         std::memcpy(out, o.data(), sizeof(double) * o.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// Timing of the reference's own calls with the value types built once outside
+// the timed region (bench.py cpu_baseline; the reference's bench does the
+// same list, bench_moeplan.cpp:128-170). Median of `reps` single-threaded runs.
+// ms[0] build_scatter_map x n, ms[1] sort_tokens_for_tiles(tile_rows) x n on
+// those maps, ms[2] balance_metrics.
+int ref_time_routing(int64_t T, int64_t E, int64_t k, int64_t n_groups, const int32_t* experts,
+                     const int32_t* src, const uint8_t* dropped, int64_t n, int64_t tile_rows,
+                     int reps, double* ms) {
+    try {
+        using clk = std::chrono::steady_clock;
+        const auto a = make_assignment(T, E, k, n_groups, experts, src, dropped);
+        std::vector<double> t0s, t1s, t2s;
+        for (int it = 0; it < reps; ++it) {
+            std::vector<routing::ScatterMap> maps;
+            auto c0 = clk::now();
+            for (int64_t r = 0; r < n; ++r) maps.push_back(routing::build_scatter_map(a, n, r));
+            auto c1 = clk::now();
+            size_t tiles = 0;
+            for (int64_t r = 0; r < n; ++r) tiles += routing::sort_tokens_for_tiles(maps[r], a, tile_rows).tiles.size();
+            auto c2 = clk::now();
+            const auto st = routing::balance_metrics(a, n);
+            auto c3 = clk::now();
+            if (tiles == 0 && st.capacity < 0) return -1;  // keep the results live
+            t0s.push_back(std::chrono::duration<double, std::milli>(c1 - c0).count());
+            t1s.push_back(std::chrono::duration<double, std::milli>(c2 - c1).count());
+            t2s.push_back(std::chrono::duration<double, std::milli>(c3 - c2).count());
+        }
+        auto med = [](std::vector<double> v) { std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+        ms[0] = med(t0s);
+        ms[1] = med(t1s);
+        ms[2] = med(t2s);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// ms[0] quantize(x, rows, cols, gran) in fmt; ms[1] emulate_reduce(vectors, kind)
+int ref_time_numerics(const double* x, int64_t rows, int64_t cols, int gran, int64_t group_size,
+                      int fmt, const double* vectors, int64_t ranks, int64_t dim, int kind, double* ms) {
+    try {
+        using clk = std::chrono::steady_clock;
+        numerics::QuantScheme s;
+        s.granularity = static_cast<numerics::Granularity>(gran);
+        s.group_size = group_size;
+        std::vector<double> v(x, x + rows * cols);
+        std::vector<std::vector<double>> vv(ranks);
+        for (int64_t r = 0; r < ranks; ++r) vv[r].assign(vectors + r * dim, vectors + (r + 1) * dim);
+        auto c0 = clk::now();
+        const auto q = numerics::quantize(v, rows, cols, s, static_cast<Format>(fmt));
+        auto c1 = clk::now();
+        const auto o = numerics::emulate_reduce(vv, static_cast<numerics::ReduceKind>(kind));
+        auto c2 = clk::now();
+        if (q.scales.empty() || o.empty()) return -1;
+        ms[0] = std::chrono::duration<double, std::milli>(c1 - c0).count();
+        ms[1] = std::chrono::duration<double, std::milli>(c2 - c1).count();
         return 0;
     } catch (const std::exception& e) {
         return status_of(e);

@@ -37,6 +37,8 @@ enum Field {
 };
 }  // namespace
 
+constexpr int kStampSlots = 64;  // PH_COUNT phase stamps + 2 per barrier slot (4 slots)
+
 enum Phase {
     PH_ROUTE, PH_PERMUTE, PH_DISPATCH, PH_FC1, PH_FC2, PH_COMBINE, PH_FWD_END,
     PH_DISPATCH_DY, PH_FC2_DGRAD, PH_FC1_DGRAD, PH_DGATE, PH_COMBINE_DX, PH_FC2_WGRAD,
@@ -127,10 +129,18 @@ struct moe_layer {
     T* const* tab(int field) const {
         return reinterpret_cast<T* const*>((comm_local ? tab_local : tab_remote) + field * n);
     }
+    // %globaltimer trace: stamps[ph] at each phase boundary, stamps[PH_COUNT +
+    // 2*slot + {0,1}] at each barrier's entry / release (captured into graphs)
+    bool stamping = false;
+    unsigned long long* stamps = nullptr;
     void mark(int ph, cudaStream_t s) {
         if (timing) {
             cudaEventRecord(ev[ph], s);
             ev_used[ph] = true;
+        }
+        if (stamping) {
+            moe::stamp_kernel<<<1, 32, 0, s>>>(stamps + ph);
+            moe::count_launch();
         }
     }
 };
@@ -244,7 +254,8 @@ moe_status build_plans(moe_layer* L) {
 void set_dispatch(moe_layer* L, GemmArgs& a, bool backward, uint16_t* dst) {
     // with peers to pull from, the first wave should need only the first 8
     // row blocks; on one GPU the whole-group raster reads each weight once
-    if (L->fused_dispatch && L->n > 1 && !L->comm_local) a.m_chunk = 8;
+    // (also in compute-only mode, so that mode runs the identical tile order)
+    if (L->fused_dispatch && L->n > 1) a.m_chunk = 8;
     a.pad_row_tok = L->pad_tok;
     a.nrows_pad = L->gpad_off + L->el;
     a.a_dst = dst;
@@ -288,7 +299,8 @@ moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
     if (L->n == 1 || L->comm_local) return MOE_OK;
     if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
     flag_barrier_kernel<<<1, 64, 0, s>>>(L->tab<uint32_t>(F_FLAGS), slot, (int)L->n, (int)L->rank,
-                                        L->epoch_dev, bump, 20ull * 1000 * 1000 * 1000, L->err);
+                                        L->epoch_dev, bump, 20ull * 1000 * 1000 * 1000, L->err,
+                                        L->stamping ? L->stamps + PH_COUNT + 2 * slot : nullptr);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;
@@ -461,6 +473,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->err, 1));
     TRY_ALLOC(dalloc(&L->epoch_dev, 1));
     TRY_ALLOC(dalloc(&L->counters, 10));
+    TRY_ALLOC(dalloc(&L->stamps, kStampSlots));
     TRY_ALLOC(dalloc(&L->router_rows, 1));
     L->norm = c.ffn_norm != 0;
     if (L->norm) {
@@ -524,7 +537,7 @@ void moe_layer_destroy(moe_layer* L) {
                     L->dgate_part, L->dlogits, L->rw_part, L->ready, L->first_row, L->dup_src, L->row_done,
                     L->tab_remote, L->tab_local,
                     L->err, L->epoch_dev, L->counters, L->router_rows, L->dlogits_bf16, L->x_res, L->dxn, L->gamma, L->rstd,
-                    L->dgamma, L->dgamma_part, L->x_all, L->ag_ready, L->inv, L->rows_out};
+                    L->dgamma, L->dgamma_part, L->x_all, L->ag_ready, L->inv, L->rows_out, L->stamps};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
@@ -1028,6 +1041,25 @@ moe_status moe_quantize_e4m3_fast(const uint16_t* d_x, int64_t rows, int64_t col
     MOE_CHECK_ARG(rows >= 0 && cols > 0 && cols % 128 == 0, "cols must be a positive multiple of 128");
     if (rows == 0) return MOE_OK;
     return quantize_rows(d_x, rows, cols, group == 0, d_codes, d_scales, (cudaStream_t)stream);
+}
+
+moe_status moe_layer_enable_stamps(moe_layer* L, int enable) {
+    MOE_CHECK_ARG(L, "null argument");
+    L->stamping = enable != 0;
+    if (L->stamping) MOE_CUDA_TRY(cudaMemset(L->stamps, 0, kStampSlots * sizeof(unsigned long long)));
+    return MOE_OK;
+}
+
+moe_status moe_layer_read_stamps(moe_layer* L, uint64_t* h_ns, int max_slots, int* n_phases,
+                                 const char** names) {
+    MOE_CHECK_ARG(L && h_ns && n_phases, "null argument");
+    MOE_CUDA_TRY(cudaDeviceSynchronize());
+    const int cnt = std::min(max_slots, kStampSlots);
+    MOE_CUDA_TRY(cudaMemcpy(h_ns, L->stamps, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    *n_phases = PH_COUNT;
+    if (names)
+        for (int i = 0; i < PH_COUNT && i < max_slots; ++i) names[i] = kPhaseNames[i];
+    return MOE_OK;
 }
 
 moe_status moe_layer_status(moe_layer* L, moe_stream_t stream) {

@@ -690,11 +690,14 @@ static __global__ void publish_meta_kernel(const int32_t* __restrict__ ex, const
 // is bumped on the device (bump = 1 at the first barrier of a pass), so the
 // whole layer can be captured once in a CUDA graph and replayed. Bounded
 // spin -> *err = 1 on timeout instead of a hang.
+// `stamp` (optional): %globaltimer at entry and at release, so the wait for the
+// slowest rank (rank-imbalance idle) is measured inside graph-replayed steps.
 static __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot, int n, int rank,
                                     uint32_t* epoch_dev, int bump, unsigned long long timeout_ns,
-                                    int* err) {
+                                    int* err, unsigned long long* stamp = nullptr) {
     __shared__ uint32_t s_epoch;
     if (threadIdx.x == 0) {
+        if (stamp) stamp[0] = globaltimer();
         uint32_t e = *epoch_dev;
         if (bump) *epoch_dev = ++e;
         s_epoch = e;
@@ -718,6 +721,12 @@ static __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot
         }
     }
     __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[1] = globaltimer();
+}
+
+// %globaltimer stamp at a phase boundary (trace of graph-replayed steps)
+static __global__ void stamp_kernel(unsigned long long* p) {
+    if (threadIdx.x == 0) *p = globaltimer();
 }
 
 // K1 fast path: router weights staged in shared memory as fp32 (E*h*4 bytes),

@@ -193,6 +193,22 @@ class MoELayer:
         check(lib().moe_layer_phase_times(self._h, ms, 32, C.byref(cnt), names))
         return {names[i].decode(): ms[i] for i in range(cnt.value)}
 
+    def enable_stamps(self, on=True):
+        """%globaltimer stamps at phase boundaries and barrier entry/release
+        (captured into CUDA graphs; see moe_layer_enable_stamps)."""
+        check(lib().moe_layer_enable_stamps(self._h, int(bool(on))))
+
+    def read_stamps(self):
+        """(phase -> ns, barrier slot -> (entry ns, release ns)) of the last step."""
+        buf = (C.c_uint64 * 64)()
+        names = (C.c_char_p * 64)()
+        cnt = C.c_int()
+        check(lib().moe_layer_read_stamps(self._h, buf, 64, C.byref(cnt), names))
+        n = cnt.value
+        phases = {names[i].decode(): int(buf[i]) for i in range(n) if buf[i]}
+        bars = {s: (int(buf[n + 2 * s]), int(buf[n + 2 * s + 1])) for s in range(4) if buf[n + 2 * s]}
+        return phases, bars
+
     def set_fused_dispatch(self, on: bool):
         check(lib().moe_layer_set_fused_dispatch(self._h, int(bool(on))))
 

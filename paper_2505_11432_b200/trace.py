@@ -42,3 +42,98 @@ def trace_events(phases_ms: dict, rows: int, h: int, f: int, exposed_comm_s: flo
 def write_trace(path: str, phases_ms: dict, rows: int, h: int, f: int, exposed_comm_s=None) -> None:
     with open(path, "w") as fh:
         json.dump(trace_events(phases_ms, rows, h, f, exposed_comm_s), fh, indent=1)
+
+
+PHASE_ORDER = ("route", "permute", "dispatch", "fc1", "fc2", "combine", "fwd_end", "dispatch_dy", "fc2_dgrad",
+               "fc1_dgrad", "dgate", "combine_dx", "fc2_wgrad", "fc1_wgrad", "router_wgrad", "end")
+# the phase whose interval contains each barrier slot's wait (layer.cu)
+BARRIER_PHASE = {0: "route", 1: "fc2", 2: "dispatch_dy", 3: "dgate"}
+
+
+def _intervals(phases_ns: dict):
+    names = [p for p in PHASE_ORDER if p in phases_ns]
+    out = []
+    for a, b in zip(names, names[1:]):
+        if a == "fwd_end":
+            continue
+        out.append((a, phases_ns[a], phases_ns[b]))
+    return out
+
+
+def stamp_summary(all_ranks: list) -> dict:
+    """%globaltimer stamps of graph-replayed steps from every rank ->
+    per-phase durations (median over steps of the max over ranks), step
+    makespan, and the flag-barrier waits (time a rank idles for the slowest
+    one: rank imbalance / skew, not link time — the fused kernels carry the
+    NVLink traffic inside the compute phases)."""
+    import numpy as np
+    nsteps = min(len(r["steps"]) for r in all_ranks)
+    per_phase, makespans, waits = {}, [], {}
+    for s in range(nsteps):
+        starts, ends = [], []
+        dur = {}
+        for r in all_ranks:
+            st = r["steps"][s]
+            iv = _intervals(st["phases"])
+            if not iv:
+                continue
+            starts.append(iv[0][1])
+            ends.append(iv[-1][2])
+            for name, a, b in iv:
+                dur.setdefault(name, []).append((b - a) / 1e6)
+            for slot, (e0, e1) in st["barriers"].items():
+                waits.setdefault(int(slot), []).append((s, (e1 - e0) / 1e6))
+        if starts:
+            makespans.append((max(ends) - min(starts)) / 1e6)
+        for name, v in dur.items():
+            per_phase.setdefault(name, []).append(max(v))
+    wait_med = {}
+    for slot, lst in waits.items():
+        by_step = {}
+        for s, w in lst:
+            by_step[s] = max(by_step.get(s, 0.0), w)
+        wait_med[slot] = float(np.median(list(by_step.values())))
+    summary = {
+        "steps": nsteps, "ranks": len(all_ranks),
+        "makespan_ms": {"median": float(np.median(makespans)), "min": float(np.min(makespans)),
+                        "max": float(np.max(makespans))} if makespans else None,
+        "phases_ms": {k: round(float(np.median(v)), 4) for k, v in per_phase.items()},
+        "barrier_wait_ms": {f"slot{k}_{BARRIER_PHASE[k]}": round(v, 4) for k, v in sorted(wait_med.items())},
+        "rank_imbalance_idle_ms": round(sum(wait_med.values()), 4),
+        "how": "device %globaltimer stamps at each phase boundary and at every flag barrier's entry/release, "
+               "inside graph-replayed steps; phase = median over steps of the max over ranks; barrier wait = "
+               "time a rank idles at the barrier for the slowest rank",
+    }
+    return {"summary": summary, "raw": all_ranks}
+
+
+def write_stamp_trace(path: str, gtrace: dict, rows: int, h: int, f: int, exposed_comm_s=None) -> None:
+    """Trace-event file (reference schema, trace.cpp:44-78) of the LAST
+    graph-replayed step: one process per rank on the shared device clock,
+    phases on the compute lane, barrier waits on comm_intra."""
+    raw = gtrace["raw"]
+    step = min(len(r["steps"]) for r in raw) - 1
+    t0 = min(min(r["steps"][step]["phases"].values()) for r in raw)
+    events = []
+    for r in raw:
+        pid = r["rank"]
+        for tid, lane in enumerate(("compute", "comm_intra", "comm_inter")):
+            events.append({"ph": "M", "pid": pid, "tid": tid, "name": "thread_name", "args": {"name": lane}})
+        st = r["steps"][step]
+        for name, a, b in _intervals(st["phases"]):
+            events.append({"ph": "X", "pid": pid, "tid": 0, "name": name, "ts": (a - t0) / 1e3,
+                           "dur": (b - a) / 1e3,
+                           "args": {"kind": KINDS.get(name, "fused"), "flops": phase_flops(name, rows, h, f),
+                                    "bytes": 0.0, "remat": name == "fc2_dgrad"}})
+        for slot, (e0, e1) in st["barriers"].items():
+            events.append({"ph": "X", "pid": pid, "tid": 1, "name": f"barrier_wait_{BARRIER_PHASE[int(slot)]}",
+                           "ts": (e0 - t0) / 1e3, "dur": (e1 - e0) / 1e3,
+                           "args": {"kind": "idle", "flops": 0.0, "bytes": 0.0, "remat": False}})
+    summ = gtrace["summary"]
+    out = {"schema_version": 1, "displayTimeUnit": "ns", "traceEvents": events,
+           "makespan_seconds": (summ["makespan_ms"]["median"] / 1e3) if summ["makespan_ms"] else 0.0,
+           "exposed_comm_seconds": exposed_comm_s,
+           "rank_imbalance_idle_seconds": summ["rank_imbalance_idle_ms"] / 1e3,
+           "summary": summ}
+    with open(path, "w") as fh:
+        json.dump(out, fh, indent=1)

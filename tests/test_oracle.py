@@ -180,3 +180,25 @@ def test_bf16_sampled_restatement_matches_dense_oracle(gate_after):
     np.testing.assert_allclose(dw2, ob["dw2"][:, :, cols].transpose(0, 2, 1), rtol=1e-4, atol=1e-6)
     dwr = P.orc_router_wgrad_from_dgates(xf, ex, gt, ob["dgates"], dr, E)
     np.testing.assert_allclose(dwr, ob["dwr"], rtol=1e-4, atol=1e-6)
+
+
+def test_numpy_blas_dense_restatement_matches_c_oracle():
+    """The numpy/BLAS dense restatement (bench.py's full-shape CPU baseline)
+    computes the same layer as the C oracle."""
+    rng = np.random.default_rng(4)
+    T, h, f, E, k = 40, 64, 96, 4, 2
+    x = rng.standard_normal((T, h)).astype(np.float32) * 0.5
+    dy = rng.standard_normal((T, h)).astype(np.float32) * 0.1
+    w1 = rng.standard_normal((E, 2 * f, h)).astype(np.float32) / 8
+    w2 = rng.standard_normal((E, h, f)).astype(np.float32) / 10
+    wr = rng.standard_normal((E, h)).astype(np.float32) / 8
+    lg, ex, gt = P.orc_router_topk(x, wr, k)
+    nlg, nex, ngt = P.np_router_topk(x, wr, k)
+    assert (nex == ex).all()
+    np.testing.assert_allclose(ngt, gt, rtol=1e-5)
+    dr = np.zeros(T, np.uint8)
+    y, dx, dg, (dw1, dw2, dwr) = P.np_moe_fwd_bwd(x, dy, wr, w1, w2, k, ex, gt, dr)
+    oy = P.orc_moe_forward(x, ex, gt, dr, w1, w2)
+    ob = P.orc_moe_backward(x, dy, ex, gt, lg, dr, w1, w2, wr)
+    for a, b in ((y, oy), (dx, ob["dx"]), (dg, ob["dgates"]), (dw1, ob["dw1"]), (dw2, ob["dw2"]), (dwr, ob["dwr"])):
+        np.testing.assert_allclose(a, b, rtol=2e-4, atol=2e-5)
