@@ -225,6 +225,24 @@ moe_status moe_layer_set_routing(moe_layer* L, const int32_t* d_experts, const f
 moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y,
                              moe_stream_t stream);
 
+/* The same forward as three operators in the reference's fused-pair
+ * structure (schedule.cpp:205-272 default_fusions; FusedPair simsched.hpp:137-145),
+ * issued in this order on one stream (moe_layer_forward == the three calls):
+ *  - moe_layer_route   K1+K2: ffn_norm?, router + top-k + gates (graph.cpp:267-271),
+ *    routing-metadata all-gather, capacity drop + build_scatter_map +
+ *    tile metadata (routing.cpp:113-187);
+ *  - moe_dispatch_fc1  K3: AG(+scatter)+GroupedGEMM: the token rows pulled over
+ *    NVLink into permuted order inside fc1, SwiGLU (+ gate) epilogue
+ *    (graph.cpp:276-295, ag_ffn_in/a2a_dispatch + scatter + fc1 + swiglu + weighted_sum);
+ *  - moe_fc2_combine   K4+K5: GroupedGEMM(+gather)+RS: fc2 whose epilogue
+ *    stores every row into its owner's staging over NVLink (or the ag_rs
+ *    pre-reduced partials), flag barrier, fixed-order combine into d_y
+ *    (graph.cpp:296-309).
+ * Errors: MOE_ERR_INVALID when called out of order. */
+moe_status moe_layer_route(moe_layer* L, const uint16_t* d_x, moe_stream_t stream);
+moe_status moe_dispatch_fc1(moe_layer* L, moe_stream_t stream);
+moe_status moe_fc2_combine(moe_layer* L, uint16_t* d_y, moe_stream_t stream);
+
 /* Backward: dx[T_r, h] from dy[T_r, h]; weight gradients written (not
  * accumulated) into dw1 [E_local][2f][h] (reference layout), dw2
  * [E_local][h][f], dwr [E][h] (fp32, this rank's tokens' contribution).

@@ -115,6 +115,7 @@ struct moe_layer {
     int* counters = nullptr;  // dynamic tile schedule counters, one per GEMM plan
     bool router_attr = false;
     bool weights_set = false, routing_set = false, fwd_done = false, ipc_ready = false;
+    int stage = 0;  // forward stages done: 1 = routed, 2 = dispatch + fc1
     // GEMM plans (tensor maps fixed at create)
     moe::GemmPlan p_fc1, p_fc2, p_fc2_dgrad, p_fc2_wgrad, p_fc1_dgrad, p_fc1_wgrad;
     // timing
@@ -585,14 +586,21 @@ moe_status moe_layer_set_routing(moe_layer* L, const int32_t* d_experts, const f
     return MOE_OK;
 }
 
-moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, moe_stream_t stream) {
-    MOE_CHECK_ARG(L && d_y, "null argument");
+// The forward in the reference's fused-pair structure (schedule.cpp:205-272):
+// K1+K2 route (router, routing-metadata all-gather, capacity drop, permutation),
+// K3 dispatch_fc1 (AG + local scatter fused into fc1 + SwiGLU + gate) and
+// K4+K5 fc2_combine (fc2 with the gather/RS epilogue, combine).
+static moe_status check_forward_args(moe_layer* L) {
+    MOE_CHECK_ARG(L, "null argument");
     MOE_CHECK_ARG(L->weights_set, "weights not set");
     MOE_CHECK_ARG(L->cfg.route_mode == 0 || L->routing_set, "injected routing not set");
     MOE_CHECK_ARG(L->n == 1 || L->ipc_ready, "ep_size > 1 requires moe_layer_ipc_import");
-    MOE_TRY(pending_timeout(L));
-    cudaStream_t s = (cudaStream_t)stream;
+    return pending_timeout(L);
+}
+
+static moe_status fwd_route(moe_layer* L, const uint16_t* d_x, cudaStream_t s) {
     const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
+    (void)Tr; (void)h; (void)f; (void)k; (void)el;
     uint16_t* x_sym = L->mine<uint16_t>(F_X);
     for (int i = 0; i < PH_COUNT; ++i) L->ev_used[i] = false;
     L->mark(PH_ROUTE, s);
@@ -687,6 +695,13 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         count_launch();
         MOE_CUDA_TRY(cudaGetLastError());
     }
+    L->stage = 1;
+    return MOE_OK;
+}
+
+static moe_status fwd_dispatch_fc1(moe_layer* L, cudaStream_t s) {
+    const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
+    (void)Tr; (void)h; (void)f; (void)k; (void)el;
     // fc1 + SwiGLU (+ gate before fc2)
     L->mark(PH_FC1, s);
     {
@@ -706,6 +721,13 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
         p.dispatch = L->fused_dispatch;
         MOE_TRY(gemm_launch(p, a, s));
     }
+    L->stage = 2;
+    return MOE_OK;
+}
+
+static moe_status fwd_fc2_combine(moe_layer* L, uint16_t* d_y, cudaStream_t s) {
+    const int64_t Tr = L->Tr, h = L->h, f = L->f, k = L->k, el = L->el;
+    (void)Tr; (void)h; (void)f; (void)k; (void)el;
     // fc2 + gather to the source rank's combine staging (bf16 or FP8 payload)
     L->mark(PH_FC2, s);
     {
@@ -750,7 +772,34 @@ moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, m
     L->mark(PH_FWD_END, s);
     MOE_TRY(mirror_error(L, s));
     L->fwd_done = true;
+    L->stage = 0;
     return MOE_OK;
+}
+
+moe_status moe_layer_forward(moe_layer* L, const uint16_t* d_x, uint16_t* d_y, moe_stream_t stream) {
+    MOE_CHECK_ARG(L && d_y, "null argument");
+    MOE_TRY(check_forward_args(L));
+    cudaStream_t s = (cudaStream_t)stream;
+    MOE_TRY(fwd_route(L, d_x, s));
+    MOE_TRY(fwd_dispatch_fc1(L, s));
+    return fwd_fc2_combine(L, d_y, s);
+}
+
+moe_status moe_layer_route(moe_layer* L, const uint16_t* d_x, moe_stream_t stream) {
+    MOE_TRY(check_forward_args(L));
+    return fwd_route(L, d_x, (cudaStream_t)stream);
+}
+
+moe_status moe_dispatch_fc1(moe_layer* L, moe_stream_t stream) {
+    MOE_CHECK_ARG(L, "null argument");
+    MOE_CHECK_ARG(L->stage == 1, "moe_dispatch_fc1 needs moe_layer_route first");
+    return fwd_dispatch_fc1(L, (cudaStream_t)stream);
+}
+
+moe_status moe_fc2_combine(moe_layer* L, uint16_t* d_y, moe_stream_t stream) {
+    MOE_CHECK_ARG(L && d_y, "null argument");
+    MOE_CHECK_ARG(L->stage == 2, "moe_fc2_combine needs moe_dispatch_fc1 first");
+    return fwd_fc2_combine(L, d_y, (cudaStream_t)stream);
 }
 
 moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d_dx,

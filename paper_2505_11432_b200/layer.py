@@ -140,6 +140,26 @@ class MoELayer:
         check(lib().moe_layer_forward(self._h, ptr(x), ptr(y), stream_ptr(stream)))
         return y
 
+    # the forward as the reference's fused pairs (moe_layer_route / moe_dispatch_fc1 /
+    # moe_fc2_combine; schedule.cpp:205-272)
+    def route(self, x: torch.Tensor | None, stream=None):
+        """K1+K2: router, routing metadata, capacity drop, permutation."""
+        if x is not None:
+            x = _check(x.contiguous(), (self.Tr, self.h), torch.bfloat16, "x")
+        check(lib().moe_layer_route(self._h, ptr(x), stream_ptr(stream)))
+
+    def dispatch_fc1(self, stream=None):
+        """K3: AG + local scatter fused into fc1 + SwiGLU (+ gate)."""
+        check(lib().moe_dispatch_fc1(self._h, stream_ptr(stream)))
+
+    def fc2_combine(self, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """K4+K5: fc2 with the gather / RS epilogue, then the combine."""
+        if y is None:
+            y = torch.empty(self.Tr, self.h, dtype=torch.bfloat16, device="cuda")
+        _check(y, (self.Tr, self.h), torch.bfloat16, "y")
+        check(lib().moe_fc2_combine(self._h, ptr(y), stream_ptr(stream)))
+        return y
+
     def backward(self, dy: torch.Tensor, dx=None, dw1=None, dw2=None, dwr=None, want_weight_grads=True,
                  dx_event: "torch.cuda.Event | None" = None, stream=None):
         """dx first (fc2 dgrad + SwiGLU bwd, fc1 dgrad + gather, combine), then

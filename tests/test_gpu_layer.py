@@ -201,3 +201,24 @@ def test_layer_experts_without_tokens(T, E, k):
     assert rel(dw2.float().cpu().numpy()[:3], ob["dw2"][:3]) < TOL
     assert dw1[3:].abs().max().item() == 0.0 and dw2[3:].abs().max().item() == 0.0
     assert rel(L.routing()["dgates"].cpu().numpy(), ob["dgates"]) < TOL
+
+
+def test_fused_pair_operators_equal_composite_forward():
+    """moe_layer_route + moe_dispatch_fc1 + moe_fc2_combine (the reference's
+    fused pairs, schedule.cpp:205-272) give exactly the composite forward;
+    calling them out of order is a domain error."""
+    from paper_2505_11432_b200 import DomainError
+    L, x, *_ = make_layer(512, 512, 768, 8, 2, seed=21)
+    y_ref = L.forward(x.cuda()).clone()
+    with pytest.raises(DomainError):
+        L.fc2_combine()
+    L.route(x.cuda())
+    with pytest.raises(DomainError):
+        L.fc2_combine()
+    L.dispatch_fc1()
+    y = L.fc2_combine()
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)
+    dy = (torch.randn(512, 512) * 0.1).bfloat16().cuda()
+    L.backward(dy)   # the staged forward leaves the layer ready for backward
+    L.status()
