@@ -35,6 +35,9 @@ CONFIGS = {
                      num_experts=256, top_k=8, tokens_per_rank=4096),
     "small": dict(workload="small-moe-layer-fwd+bwd", hidden=1024, ffn_hidden=2816,
                   num_experts=8, top_k=2, tokens_per_rank=4096),
+    # configs[0] as BASELINE states it: fp32 forward on one GPU (FFMA grouped GEMMs)
+    "small_f32": dict(workload="small-moe-layer-fwd-fp32", hidden=1024, ffn_hidden=2816,
+                      num_experts=8, top_k=2, tokens_per_rank=4096),
     # configs[4]: Mixtral shape, FP8 dispatch/combine, gate after fc2,
     # Zipf(1.2) routing from the reference's own simulate_routing (golden fixture)
     "mixtral_fp8_zipf": dict(workload="mixtral-8x7b-moe-layer-fwd+bwd-fp8comm-zipf1.2", hidden=4096,
@@ -127,6 +130,43 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(s[1] for s in self.samples) if self.samples else None,
                 "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
+
+
+class NvlinkCounters:
+    """Cumulative NVLink data bytes of one GPU from NVML field values
+    (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX, KiB, summed over links):
+    read before and after a timed region, they give the bytes the fused
+    kernels actually put on the links (payload, no protocol overhead)."""
+
+    TX, RX = 138, 139
+
+    def __init__(self, gpu_index: int):
+        import pynvml as N
+        N.nvmlInit()
+        self.N = N
+        self.hd = N.nvmlDeviceGetHandleByIndex(gpu_index)
+        self.links = []
+        for link in range(18):
+            try:
+                if N.nvmlDeviceGetNvLinkState(self.hd, link) == N.NVML_FEATURE_ENABLED:
+                    self.links.append(link)
+            except Exception:
+                pass
+
+    def read(self):
+        N = self.N
+        tx = rx = 0
+        for link in self.links:
+            vals = N.nvmlDeviceGetFieldValues(self.hd, [(self.TX, link), (self.RX, link)])
+            for v, acc in zip(vals, ("tx", "rx")):
+                if v.nvmlReturn != 0:
+                    continue
+                x = getattr(v.value, "ullVal", 0) or getattr(v.value, "ulVal", 0)
+                if acc == "tx":
+                    tx += x
+                else:
+                    rx += x
+        return tx * 1024, rx * 1024
 
 
 _CPU_STATE = {}
@@ -330,6 +370,13 @@ def run_ours(args, cfg):
         run_step = graph.replay
 
     # ---- device-timed region (inputs resident in HBM) ----
+    nvl = None
+    if world > 1:
+        try:
+            nvl = NvlinkCounters(local)
+        except Exception:  # noqa: BLE001
+            nvl = None
+    nvl0 = nvl.read() if nvl else None
     clocks = ClockSampler(local)
     clocks.start()
     launch_count_reset()
@@ -342,6 +389,10 @@ def run_ours(args, cfg):
     sync_all()
     launches = launch_count() if args.no_graph else per_step_launches * args.steps
     clk = clocks.stop()
+    nvl_meas = None
+    if nvl:
+        tx1, rx1 = nvl.read()
+        nvl_meas = [(tx1 - nvl0[0]) / args.steps, (rx1 - nvl0[1]) / args.steps]
     ms_local = ev0.elapsed_time(ev1) / args.steps
     t = torch.tensor([ms_local], device="cuda")
     if world > 1:
@@ -592,7 +643,18 @@ def run_ours(args, cfg):
             fwd_b = ((n - 1) * Tr + rs_rows) * h * bpe
             bwd_b = fwd_b
             pulled_fwd = (n - 1) * Tr
-        nvlink = {"remote_rows": remote_rows, "remote_tokens": remote_tokens, "rows_pulled": pulled_fwd,
+        measured = None
+        allm = [None] * world
+        dist.all_gather_object(allm, nvl_meas)
+        if all(m_ is not None for m_ in allm):
+            tx_max = max(m_[0] for m_ in allm)
+            rx_max = max(m_[1] for m_ in allm)
+            measured = {"source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX over the timed region, per rank per step",
+                        "tx_bytes_per_step_per_rank": [m_[0] for m_ in allm],
+                        "rx_bytes_per_step_per_rank": [m_[1] for m_ in allm],
+                        "max_GBps_tx": tx_max / (ms / 1000.0) / 1e9, "max_GBps_rx": rx_max / (ms / 1000.0) / 1e9,
+                        "frac_900_over_step": max(tx_max, rx_max) / (ms / 1000.0) / 900e9}
+        nvlink = {"measured_nvml": measured, "remote_rows": remote_rows, "remote_tokens": remote_tokens, "rows_pulled": pulled_fwd,
                   "bytes_per_step": fwd_b + bwd_b,
                   "link_GBps_if_spread_over_step": (fwd_b + bwd_b) / (ms / 1000.0) / 1e9,
                   "link_time_ms_at_770GBps": (fwd_b + bwd_b) / 770e9 * 1000.0,
@@ -713,6 +775,67 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_f32(args, cfg):
+    """configs[0]: the fp32 layer forward (router, capacity drop, permutation,
+    FFMA expert GEMMs, SwiGLU, combine) on one GPU, against the FFMA roofline
+    (148 SMs x 128 fp32 lanes x 2 FLOP x SM clock)."""
+    import torch
+    from paper_2505_11432_b200 import launch_count, launch_count_reset, ops
+    torch.cuda.set_device(0)
+    h, f, E, k, T = cfg["hidden"], cfg["ffn_hidden"], cfg["num_experts"], cfg["top_k"], cfg["tokens_per_rank"]
+    g = torch.Generator(device="cuda").manual_seed(42)
+    w1 = torch.randn(E, 2 * f, h, device="cuda", generator=g) / h ** 0.5
+    w2 = torch.randn(E, h, f, device="cuda", generator=g) / f ** 0.5
+    wr = torch.randn(E, h, device="cuda", generator=g) / h ** 0.5
+    x = torch.randn(T, h, device="cuda", generator=g) * 0.5
+    for _ in range(args.warmup):
+        ops.ffn_forward_f32(x, w1, w2, wr, k)
+    torch.cuda.synchronize()
+    launch_count_reset()
+    ops.ffn_forward_f32(x, w1, w2, wr, k)
+    torch.cuda.synchronize()
+    per_step = launch_count()
+    clocks = ClockSampler(0)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        ops.ffn_forward_f32(x, w1, w2, wr, k)
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    # e2e: host x in, host y out, through the public operator
+    xh = x.cpu().pin_memory()
+    yh = torch.empty(T, h, dtype=torch.float32).pin_memory()
+    e0.record()
+    for _ in range(args.steps):
+        xd = xh.to("cuda", non_blocking=True)
+        y = ops.ffn_forward_f32(xd, w1, w2, wr, k)[0]
+        yh.copy_(y, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    flops = 2.0 * T * k * h * 2 * f + 2.0 * T * k * f * h + 2.0 * T * h * E
+    mhz = clk["sm_mhz"] or 1965.0
+    ffma_peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+    line = {
+        "metric": "moe_layer_fwd_tokens_per_s", "value": T / (ms / 1000.0), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights)",
+        "config": {"workload": cfg["workload"], "hidden": h, "ffn_hidden": f, "num_experts": E, "top_k": k,
+                   "tokens": T, "l2": "weights 277 MB > L2"},
+        "roofline": {"bound": "ffma", "achieved": flops / (ms / 1000.0) / 1e12, "peak": ffma_peak,
+                     "unit": "TFLOP/s", "frac": flops / (ms / 1000.0) / 1e12 / ffma_peak, "traffic": None,
+                     "peak_kind": "derived FFMA peak at the measured median SM clock (148 x 128 x 2 x clock)",
+                     "roofline_ms": flops / (ffma_peak * 1e12) * 1000.0},
+        "e2e": {"value": T / (e2e_ms / 1000.0), "unit": "tokens/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": T * h * 4, "d2h_bytes_per_step": T * h * 4},
+        "clocks": clk, "gpu_launches": int(per_step * args.steps), "gpu_launches_per_step": int(per_step),
+    }
+    print(json.dumps(line), flush=True)
 
 
 def run_attn(args, cfg):
@@ -1057,6 +1180,8 @@ def main():
         run_dp(args, cfg)
     elif args.config == "attn":
         run_attn(args, cfg)
+    elif args.config == "small_f32":
+        run_f32(args, cfg)
     else:
         run_ours(args, cfg)
 

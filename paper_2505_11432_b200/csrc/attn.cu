@@ -199,6 +199,10 @@ moe_status moe_attn_ag_gemm(moe_attn* A, const uint16_t* d_x_shard, uint16_t* d_
     a.out = d_qkv;
     a.ldo = A->nq;
     a.m_chunk = 4;  // first wave waits for 4 row blocks, not the whole gather
+    // start on this rank's own shard, then the next rank's (rotation): the first
+    // wave needs no peer rows and every rank pulls from a different peer at a time
+    a.m_rot = (int)(A->rank * A->sr / (128 * A->cg));
+    a.row_rot = (int)(A->rank * A->sr);
     a.pad_row_tok = A->ident;
     a.nrows_pad = A->rows_pad;
     a.src_bufs = reinterpret_cast<const uint16_t* const*>(A->tab);
@@ -228,6 +232,8 @@ moe_status moe_attn_gemm_rs(moe_attn* A, const uint16_t* d_o, uint16_t* d_y_shar
     a.ldo = A->h;
     a.row_dst = A->row_dst;
     a.rank_base = reinterpret_cast<void* const*>(A->tab + A->n);
+    // own rows first, then owner rank+1, ...: at any time the ranks push to different owners
+    a.m_rot = (int)(A->rank * A->sr / (128 * A->cg));
     MOE_TRY(gemm_launch(p, a, s));
     MOE_TRY(attn_barrier(A, 2, s));
     launch_combine<false>(s, 

@@ -66,6 +66,9 @@ struct GemmArgs {
     int m_chunk;                // M-grouped raster: m-tiles per chunk (0 = whole group, m fastest).
                                 // Fused-dispatch GEMMs use small chunks so the first wave only
                                 // needs the first rows to arrive.
+    int m_rot;                  // M-grouped: m-tiles are taken starting at m-tile m_rot (cyclic) —
+                                // TP AG-GEMM / GEMM-RS start on this rank's own sequence shard
+    int row_rot;                // fused dispatch: rows are claimed starting at row row_rot (cyclic)
     int interleave_rows;        // K-grouped STORE: map packed a/b-interleaved rows back to
                                 // the reference [a | b] row order (dW1)
     // fused dispatch (AG + local scatter into the A operand, DISPATCH = true)
@@ -161,6 +164,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
         const int cm = min(mc, mt - c * mc);
         ti.n = r / cm;
         ti.m = c * mc + (r - ti.n * cm);
+        if (a.m_rot) ti.m = (ti.m + a.m_rot) % mt;
         ti.kblocks = (a.K + 63) / 64;
         ti.row0 = row_off[lo] + ti.m * TILE_M;
         ti.half_tile = TILE_M == 256 && ti.m * TILE_M + TILE_M > rows;
@@ -606,7 +610,7 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int lane
             const int src = (a.self_rank + 1 + pi) % a.n_src;
             const uint4* sp = reinterpret_cast<const uint4*>(a.src_bufs[src] + (int64_t)tl * K);
             uint4* dp = reinterpret_cast<uint4*>(a.ag_dst + ((int64_t)src * Tr + tl) * K);
-            constexpr int U = 16;
+            constexpr int U = 8;   // 4 KB per warp in flight (16 would spill: comm warps share the 168-reg cap)
             for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
                 uint4 r[U];
 #pragma unroll
@@ -622,7 +626,8 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int lane
         continue;
     }
     const int claim_end = min(base + CLAIM, nag + total) - nag;
-    for (int pp = base - nag; pp < claim_end; ++pp) {
+    for (int pq = base - nag; pq < claim_end; ++pq) {
+        const int pp = a.row_rot ? (pq + a.row_rot) % total : pq;
         const int i = a.pad_row_tok[pp];
         uint4* d = reinterpret_cast<uint4*>(a.a_dst + (int64_t)pp * K);
         const int ds = (a.dup_src && i >= 0) ? a.dup_src[pp] : -1;

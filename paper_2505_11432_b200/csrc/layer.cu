@@ -113,6 +113,10 @@ struct moe_layer {
     int* err_host = nullptr;  // pinned mirror of *err, refreshed at the end of multi-GPU calls
     uint32_t* epoch_dev = nullptr;
     int* counters = nullptr;  // dynamic tile schedule counters, one per GEMM plan
+    // E <= 8 router: h split over router_split CTAs per 16-token block
+    int router_split = 1;
+    float* router_part = nullptr;
+    unsigned* router_cnt = nullptr;
     bool router_attr = false;
     bool weights_set = false, routing_set = false, fwd_done = false, ipc_ready = false;
     int stage = 0;  // forward stages done: 1 = routed, 2 = dispatch + fc1
@@ -475,6 +479,16 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->epoch_dev, 1));
     TRY_ALLOC(dalloc(&L->counters, 10));
     TRY_ALLOC(dalloc(&L->stamps, kStampSlots));
+    if (L->E <= 8 && h % 256 == 0) {
+        L->router_split = h % 1024 == 0 ? 4 : (h % 512 == 0 ? 2 : 1);
+        if (const char* e = getenv("MOE_ROUTER_SPLIT")) {
+            const int v = atoi(e);
+            if (v == 1 || (v == 2 && h % 512 == 0) || (v == 4 && h % 1024 == 0)) L->router_split = v;
+        }
+        TRY_ALLOC(dalloc(&L->router_part, (Tr + 15) / 16 * L->router_split * 128));
+        TRY_ALLOC(dalloc(&L->router_cnt, (Tr + 15) / 16));
+        cudaMemset(L->router_cnt, 0, (Tr + 15) / 16 * sizeof(unsigned));
+    }
     TRY_ALLOC(dalloc(&L->router_rows, 1));
     L->norm = c.ffn_norm != 0;
     if (L->norm) {
@@ -538,7 +552,7 @@ void moe_layer_destroy(moe_layer* L) {
                     L->dgate_part, L->dlogits, L->rw_part, L->ready, L->first_row, L->dup_src, L->row_done,
                     L->tab_remote, L->tab_local,
                     L->err, L->epoch_dev, L->counters, L->router_rows, L->dlogits_bf16, L->x_res, L->dxn, L->gamma, L->rstd,
-                    L->dgamma, L->dgamma_part, L->x_all, L->ag_ready, L->inv, L->rows_out, L->stamps};
+                    L->dgamma, L->dgamma_part, L->x_all, L->ag_ready, L->inv, L->rows_out, L->stamps, L->router_part, L->router_cnt};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int i = 0; i < PH_COUNT; ++i)
@@ -629,8 +643,10 @@ static moe_status fwd_route(moe_layer* L, const uint16_t* d_x, cudaStream_t s) {
             MOE_TRY(gemm_launch(L->p_router, a, s));
             MOE_TRY(launch_topk_from_logits(L->logits, Tr, L->E, k, L->ex_loc, L->gt_loc, s));
         } else if (L->E <= 8 && h % 256 == 0) {
-            router_logits_mma_kernel<<<(unsigned)((Tr + 15) / 16), 256, 0, s>>>(
-                x_sym, L->wr, (int)Tr, (int)h, (int)L->E, L->logits, (int)k, L->ex_loc, L->gt_loc);
+            const int ns = L->router_split;
+            router_logits_mma_kernel<<<(unsigned)((Tr + 15) / 16 * ns), 256, 0, s>>>(
+                x_sym, L->wr, (int)Tr, (int)h, (int)L->E, L->logits, (int)k, L->ex_loc, L->gt_loc, ns,
+                L->router_part, L->router_cnt);
             count_launch();
         } else if (wbytes <= 200 * 1024) {
             if (!L->router_attr) {

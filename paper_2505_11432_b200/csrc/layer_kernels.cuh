@@ -857,15 +857,24 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// nsplit > 1: the h columns of a 16-token block are split over nsplit CTAs
+// (4096 tokens -> 256 x nsplit CTAs: several per SM, so HBM sees enough
+// requests in flight); each writes its fp32 partial sums to part[] and the
+// last CTA to arrive (counter cnt[block], reset by it) adds the partials in
+// split order — deterministic whatever the arrival order — then runs the
+// top-k + softmax.
 static __global__ void __launch_bounds__(256) router_logits_mma_kernel(
     const uint16_t* __restrict__ x, const uint16_t* __restrict__ wr, int T, int h, int E,
-    float* __restrict__ logits, int k, int32_t* __restrict__ experts, float* __restrict__ gates) {
+    float* __restrict__ logits, int k, int32_t* __restrict__ experts, float* __restrict__ gates,
+    int nsplit = 1, float* __restrict__ part = nullptr, unsigned* __restrict__ cnt = nullptr) {
     __shared__ float red[8][16][8];
     __shared__ float s_lg[16][8];
+    __shared__ int s_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, c = lane & 3;
-    const int t0 = blockIdx.x * 16;
-    const int slice = h / 8, k_lo = warp * slice;
+    const int blk = blockIdx.x / nsplit, sp = blockIdx.x - blk * nsplit;
+    const int t0 = blk * 16;
+    const int slice = h / (8 * nsplit), k_lo = sp * (h / nsplit) + warp * slice;
     const bool r0 = t0 + g < T, r1 = t0 + g + 8 < T, ev = g < E;
     const uint4* xa = reinterpret_cast<const uint4*>(x + (int64_t)(t0 + g) * h + k_lo) + c;
     const uint4* xb = reinterpret_cast<const uint4*>(x + (int64_t)(t0 + g + 8) * h + k_lo) + c;
@@ -908,8 +917,28 @@ static __global__ void __launch_bounds__(256) router_logits_mma_kernel(
         float sum = red[0][r][e];
 #pragma unroll
         for (int w = 1; w < 8; ++w) sum += red[w][r][e];
-        s_lg[r][e] = sum;
-        if (e < E && t0 + r < T) logits[(int64_t)(t0 + r) * E + e] = sum;
+        if (nsplit == 1) {
+            s_lg[r][e] = sum;
+            if (e < E && t0 + r < T) logits[(int64_t)(t0 + r) * E + e] = sum;
+        } else {
+            part[((int64_t)blk * nsplit + sp) * 128 + threadIdx.x] = sum;
+            __threadfence();
+        }
+    }
+    if (nsplit > 1) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(&cnt[blk], 1u) == (unsigned)(nsplit - 1);
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        if (threadIdx.x < 128) {
+            const int r = threadIdx.x >> 3, e = threadIdx.x & 7;
+            float sum = __ldcg(part + (int64_t)blk * nsplit * 128 + threadIdx.x);
+            for (int q = 1; q < nsplit; ++q) sum += __ldcg(part + ((int64_t)blk * nsplit + q) * 128 + threadIdx.x);
+            s_lg[r][e] = sum;
+            if (e < E && t0 + r < T) logits[(int64_t)(t0 + r) * E + e] = sum;
+        }
+        if (threadIdx.x == 0) cnt[blk] = 0u;   // ready for the next call (graph replays)
     }
     __syncthreads();
     // top-k + softmax of the CTA's 16 tokens, two per warp (the separate
