@@ -104,6 +104,9 @@ struct moe_layer {
     // x_all, local scatter from it; expert outputs stored locally, pre-reduced
     // per (token, rank) and reduce-scattered to the owner
     bool ag = false;
+    // MOE_DEBUG_CHECKS=1: device-side protocol assertions (barrier epochs, dispatch
+    // arrivals) that set the error flag; moe_layer_status reports them
+    bool debug = false;
     uint16_t* x_all = nullptr;      // [T, h] (x in forward, dy in backward)
     uint32_t* ag_ready = nullptr;   // [n][ceil(T_r/64)] rows landed per 64-token chunk
     int32_t* inv = nullptr;         // [T*k] padded row of (t, slot), -1 = not here
@@ -305,7 +308,21 @@ moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
     if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
     flag_barrier_kernel<<<1, 64, 0, s>>>(L->tab<uint32_t>(F_FLAGS), slot, (int)L->n, (int)L->rank,
                                         L->epoch_dev, bump, 20ull * 1000 * 1000 * 1000, L->err,
-                                        L->stamping ? L->stamps + PH_COUNT + 2 * slot : nullptr);
+                                        L->stamping ? L->stamps + PH_COUNT + 2 * slot : nullptr, (int)L->debug);
+    count_launch();
+    MOE_CUDA_TRY(cudaGetLastError());
+    return MOE_OK;
+}
+
+// debug mode: the fused-dispatch protocol invariants after a fused GEMM
+moe_status debug_check_dispatch(moe_layer* L, bool backward, cudaStream_t s) {
+    if (!L->debug || !L->fused_dispatch) return MOE_OK;
+    const bool dd = L->dedup && !(backward && L->gate_after);
+    dispatch_check_kernel<<<kNumSMs, 256, 0, s>>>(
+        L->ready, (int)(L->Mp / L->pad + 1), L->gpad_off + L->el,
+        reinterpret_cast<const int*>(L->ready + L->Mp / L->pad + 1), L->ag ? (int)((L->n - 1) * L->Tr) : 0,
+        dd ? L->row_done : nullptr, L->pad_tok, L->ag ? L->ag_ready : nullptr, (int)L->n, (int)L->rank,
+        (int)L->Tr, L->err);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;
@@ -326,6 +343,7 @@ moe_status launch_gather_rs(moe_layer* L, cudaStream_t s) {
 moe_status pending_timeout(moe_layer* L) {
     const int v = *reinterpret_cast<volatile int*>(L->err_host);
     if (v == 0) return MOE_OK;
+    if (v >= 8) return set_error(MOE_ERR_INTERNAL, "moe_layer: debug-mode protocol assertion %d in an earlier call", v);
     return set_error(MOE_ERR_TIMEOUT, "moe_layer: an earlier call's cross-GPU wait timed out (kind %d); "
                      "its results are invalid (moe_layer_clear_error resets)", v);
 }
@@ -480,7 +498,9 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     TRY_ALLOC(dalloc(&L->counters, 10));
     TRY_ALLOC(dalloc(&L->stamps, kStampSlots));
     if (L->E <= 8 && h % 256 == 0) {
-        L->router_split = h % 1024 == 0 ? 4 : (h % 512 == 0 ? 2 : 1);
+        // default 1: the split (2 or 4 CTAs per 16-token block) measured slower at the
+        // Mixtral shape (ncu 22 vs 13 us at 4 CTAs: 3.5 waves at 2 CTAs/SM)
+        L->router_split = 1;
         if (const char* e = getenv("MOE_ROUTER_SPLIT")) {
             const int v = atoi(e);
             if (v == 1 || (v == 2 && h % 512 == 0) || (v == 4 && h % 1024 == 0)) L->router_split = v;
@@ -519,6 +539,7 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     // on by default (DeepSeek shape, EP = 4: 9.17 -> 8.93 ms per step with the
     // dynamic tile schedule; Mixtral EP = 4 unchanged); MOE_NO_DISPATCH_DEDUP=1 off
     L->dedup = L->n > 1 && L->k > 1 && L->el > 1 && !L->ag && getenv("MOE_NO_DISPATCH_DEDUP") == nullptr;
+    L->debug = getenv("MOE_DEBUG_CHECKS") != nullptr && atoi(getenv("MOE_DEBUG_CHECKS")) != 0;
     // zero the permuted buffers once so never-written rows are finite
     cudaMemset(L->x_perm, 0, Mp * h * 2);
     cudaMemset(L->dy_perm, 0, Mp * h * 2);
@@ -737,6 +758,7 @@ static moe_status fwd_dispatch_fc1(moe_layer* L, cudaStream_t s) {
         p.dispatch = L->fused_dispatch;
         MOE_TRY(gemm_launch(p, a, s));
     }
+    MOE_TRY(debug_check_dispatch(L, false, s));
     L->stage = 2;
     return MOE_OK;
 }
@@ -882,6 +904,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         p.dispatch = L->fused_dispatch;
         MOE_TRY(gemm_launch(p, a, s));
     }
+    MOE_TRY(debug_check_dispatch(L, true, s));
     // fc1 dgrad + gather of dx rows to the owning rank (GEMM + RS)
     L->mark(PH_FC1_DGRAD, s);
     {

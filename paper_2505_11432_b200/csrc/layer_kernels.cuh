@@ -694,7 +694,7 @@ static __global__ void publish_meta_kernel(const int32_t* __restrict__ ex, const
 // slowest rank (rank-imbalance idle) is measured inside graph-replayed steps.
 static __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot, int n, int rank,
                                     uint32_t* epoch_dev, int bump, unsigned long long timeout_ns,
-                                    int* err, unsigned long long* stamp = nullptr) {
+                                    int* err, unsigned long long* stamp = nullptr, int debug = 0) {
     __shared__ uint32_t s_epoch;
     if (threadIdx.x == 0) {
         if (stamp) stamp[0] = globaltimer();
@@ -722,6 +722,41 @@ static __global__ void flag_barrier_kernel(uint32_t* const* peer_flags, int slot
     }
     __syncthreads();
     if (stamp && threadIdx.x == 0) stamp[1] = globaltimer();
+    // debug mode (err != nullptr and debug): after the release every peer's flag of
+    // this slot must hold exactly this epoch — older means the wait was broken,
+    // newer means a peer ran ahead into the next use of the slot
+    if (debug && i < n) {
+        const uint32_t v = ld_acquire_sys(peer_flags[rank] + slot * 64 + i);
+        if (v != epoch) atomicExch(err, 16 + slot);
+    }
+}
+
+// Debug-mode check of the fused-dispatch protocol after a fused GEMM: every
+// 128-row block of the permuted operand received exactly 128 arrivals (each
+// padded row claimed and landed once), no block past the end received any,
+// the row-claim counter passed the end, deduplicated rows landed exactly once,
+// and (ag_rs) every all-gather chunk of every peer landed completely.
+static __global__ void dispatch_check_kernel(const uint32_t* __restrict__ ready, int nblocks_alloc,
+                                             const int32_t* nrows_pad, const int* row_claim, int ag_rows,
+                                             const uint32_t* __restrict__ row_done, const int32_t* __restrict__ pad_tok,
+                                             const uint32_t* __restrict__ ag_ready, int n, int self, int tokens_per_rank,
+                                             int* err) {
+    const int total = *nrows_pad;
+    const int nb = total / 128;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nblocks_alloc; b += gridDim.x * blockDim.x)
+        if (ready[b] != (b < nb ? 128u : 0u)) atomicExch(err, 8);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && *row_claim < ag_rows + total) atomicExch(err, 9);
+    if (row_done)
+        for (int pp = blockIdx.x * blockDim.x + threadIdx.x; pp < total; pp += gridDim.x * blockDim.x)
+            if (pad_tok[pp] >= 0 && row_done[pp] != 1u) atomicExch(err, 10);
+    if (ag_ready) {
+        const int nch = (tokens_per_rank + 63) / 64;
+        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n * nch; c += gridDim.x * blockDim.x) {
+            const int src = c / nch, ch = c - src * nch;
+            const uint32_t want = src == self ? 0u : (uint32_t)min(64, tokens_per_rank - ch * 64);
+            if (ag_ready[c] != want) atomicExch(err, 11);
+        }
+    }
 }
 
 // %globaltimer stamp at a phase boundary (trace of graph-replayed steps)

@@ -66,6 +66,11 @@ moe_status flag_status(const int* d_err, cudaStream_t s, const char* what) {
     int v = 0;
     MOE_CUDA_TRY(cudaMemcpy(&v, d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (v == 0) return MOE_OK;
+    if (v >= 8)
+        return set_error(MOE_ERR_INTERNAL, "%s: debug-mode protocol assertion failed (code %d: %s)", what, v,
+                         v == 8 ? "dispatch block arrivals != 128" : v == 9 ? "row claims did not reach the end"
+                         : v == 10 ? "deduplicated row not landed exactly once" : v == 11 ? "all-gather chunk incomplete"
+                         : "barrier epoch mismatch (16 + slot)");
     static const char* kinds[] = {"", "cross-GPU flag barrier", "fused-dispatch row arrival",
                                   "DP in-place cast chunk"};
     return set_error(MOE_ERR_TIMEOUT, "%s: a %s wait exceeded its bound (a peer rank stalled or "

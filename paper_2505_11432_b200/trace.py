@@ -68,25 +68,39 @@ def stamp_summary(all_ranks: list) -> dict:
     NVLink traffic inside the compute phases)."""
     import numpy as np
     nsteps = min(len(r["steps"]) for r in all_ranks)
-    per_phase, makespans, waits = {}, [], {}
+    per_phase, busy_phase, makespans, waits = {}, {}, [], {}
     for s in range(nsteps):
         starts, ends = [], []
-        dur = {}
+        dur, busy = {}, {}
         for r in all_ranks:
             st = r["steps"][s]
             iv = _intervals(st["phases"])
             if not iv:
                 continue
-            starts.append(iv[0][1])
-            ends.append(iv[-1][2])
-            for name, a, b in iv:
-                dur.setdefault(name, []).append((b - a) / 1e6)
+            # the GPUs' %globaltimer clocks are not aligned: put every rank on
+            # rank 0's clock through the first barrier's release, which all
+            # ranks leave at the same physical time (to within the flag latency)
+            off = 0
+            b0 = st["barriers"].get("0") or st["barriers"].get(0)
+            r0 = all_ranks[0]["steps"][s]["barriers"]
+            b0_ref = r0.get("0") or r0.get(0)
+            if b0 and b0_ref:
+                off = b0_ref[1] - b0[1]
+            starts.append(iv[0][1] + off)
+            ends.append(iv[-1][2] + off)
+            wait_in = {}
             for slot, (e0, e1) in st["barriers"].items():
                 waits.setdefault(int(slot), []).append((s, (e1 - e0) / 1e6))
+                wait_in[BARRIER_PHASE[int(slot)]] = (e1 - e0) / 1e6
+            for name, a, b in iv:
+                dur.setdefault(name, []).append((b - a) / 1e6)
+                busy.setdefault(name, []).append((b - a) / 1e6 - wait_in.get(name, 0.0))
         if starts:
             makespans.append((max(ends) - min(starts)) / 1e6)
         for name, v in dur.items():
             per_phase.setdefault(name, []).append(max(v))
+        for name, v in busy.items():
+            busy_phase.setdefault(name, []).append(max(v))
     wait_med = {}
     for slot, lst in waits.items():
         by_step = {}
@@ -98,11 +112,14 @@ def stamp_summary(all_ranks: list) -> dict:
         "makespan_ms": {"median": float(np.median(makespans)), "min": float(np.min(makespans)),
                         "max": float(np.max(makespans))} if makespans else None,
         "phases_ms": {k: round(float(np.median(v)), 4) for k, v in per_phase.items()},
+        "phases_busy_ms": {k: round(float(np.median(v)), 4) for k, v in busy_phase.items()},
         "barrier_wait_ms": {f"slot{k}_{BARRIER_PHASE[k]}": round(v, 4) for k, v in sorted(wait_med.items())},
         "rank_imbalance_idle_ms": round(sum(wait_med.values()), 4),
         "how": "device %globaltimer stamps at each phase boundary and at every flag barrier's entry/release, "
-               "inside graph-replayed steps; phase = median over steps of the max over ranks; barrier wait = "
-               "time a rank idles at the barrier for the slowest rank",
+               "inside graph-replayed steps (each replay synchronised and read back); ranks aligned on the first "
+               "barrier's release; phase = median over steps of the max over ranks; phases_busy = the same minus "
+               "the barrier wait inside the phase; barrier wait = time a rank idles at the barrier for the "
+               "slowest rank (rank imbalance / skew)",
     }
     return {"summary": summary, "raw": all_ranks}
 
@@ -113,21 +130,30 @@ def write_stamp_trace(path: str, gtrace: dict, rows: int, h: int, f: int, expose
     phases on the compute lane, barrier waits on comm_intra."""
     raw = gtrace["raw"]
     step = min(len(r["steps"]) for r in raw) - 1
-    t0 = min(min(r["steps"][step]["phases"].values()) for r in raw)
+
+    def offset(r):
+        b = r["steps"][step]["barriers"]
+        b0 = b.get("0") or b.get(0)
+        r0 = raw[0]["steps"][step]["barriers"]
+        ref = r0.get("0") or r0.get(0)
+        return (ref[1] - b0[1]) if (b0 and ref) else 0
+
+    t0 = min(min(r["steps"][step]["phases"].values()) + offset(r) for r in raw)
     events = []
     for r in raw:
         pid = r["rank"]
+        t0r = t0 - offset(r)
         for tid, lane in enumerate(("compute", "comm_intra", "comm_inter")):
             events.append({"ph": "M", "pid": pid, "tid": tid, "name": "thread_name", "args": {"name": lane}})
         st = r["steps"][step]
         for name, a, b in _intervals(st["phases"]):
-            events.append({"ph": "X", "pid": pid, "tid": 0, "name": name, "ts": (a - t0) / 1e3,
+            events.append({"ph": "X", "pid": pid, "tid": 0, "name": name, "ts": (a - t0r) / 1e3,
                            "dur": (b - a) / 1e3,
                            "args": {"kind": KINDS.get(name, "fused"), "flops": phase_flops(name, rows, h, f),
                                     "bytes": 0.0, "remat": name == "fc2_dgrad"}})
         for slot, (e0, e1) in st["barriers"].items():
             events.append({"ph": "X", "pid": pid, "tid": 1, "name": f"barrier_wait_{BARRIER_PHASE[int(slot)]}",
-                           "ts": (e0 - t0) / 1e3, "dur": (e1 - e0) / 1e3,
+                           "ts": (e0 - t0r) / 1e3, "dur": (e1 - e0) / 1e3,
                            "args": {"kind": "idle", "flops": 0.0, "bytes": 0.0, "remat": False}})
     summ = gtrace["summary"]
     out = {"schema_version": 1, "displayTimeUnit": "ns", "traceEvents": events,

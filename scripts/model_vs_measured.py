@@ -29,7 +29,7 @@ FWD_ROWS = [
      ["ag_ffn_in", "a2a_dispatch", "scatter", "fc1", "swiglu", "weighted_sum",
       "ag_ffn_in+fc1", "a2a_dispatch+fc1"], ["dispatch", "fc1"]),
     ("combine: fc2 + gather + RS/A2A", ["fc2", "gather", "rs_ffn_out", "a2a_combine",
-                                        "fc2+rs_ffn_out", "fc2+a2a_combine"], ["fc2", "combine"]),
+                                        "rs_ffn_out+fc2", "a2a_combine+fc2"], ["fc2", "combine"]),
 ]
 BWD_ROWS = [
     ("fc2 backward: dy AG/A2A + gather_bwd + remat fc2_in + dgrad/wgrad + SwiGLU/gate bwd",
@@ -59,7 +59,8 @@ def diff(bench: dict, peaks: dict) -> tuple[list, dict]:
     cfg = bench["config"]
     n = bench["n_gpus"]
     m = run_model(cfg, n, cfg.get("ep_pattern", "a2a"), cfg.get("comm_format", "bf16"), peaks)
-    meas = (bench.get("graph_trace") or {}).get("phases_ms") or bench["phases_ms"]
+    gt = bench.get("graph_trace") or {}
+    meas = gt.get("phases_busy_ms") or gt.get("phases_ms") or bench["phases_ms"]
     rows = []
     for phase, table in (("forward", FWD_ROWS), ("backward", BWD_ROWS)):
         tl = m[phase]["fused"]

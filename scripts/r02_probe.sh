@@ -10,6 +10,7 @@ for i in 1 2; do
   timeout 300 $B > $O/bench_default_$i.log 2>&1
   MOE_UNFUSED_DISPATCH=1 timeout 300 $B > $O/bench_unfused_$i.log 2>&1
   MOE_ROUTER_SPLIT=1 timeout 300 $B > $O/bench_split1_$i.log 2>&1
+  timeout 300 $B --no-graph > $O/bench_nograph_$i.log 2>&1
 done
 timeout 300 python bench.py --config small_f32 > $O/bench_small_f32.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:grouped_gemm -s 6 -c 6 \

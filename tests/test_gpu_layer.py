@@ -222,3 +222,16 @@ def test_fused_pair_operators_equal_composite_forward():
     dy = (torch.randn(512, 512) * 0.1).bfloat16().cuda()
     L.backward(dy)   # the staged forward leaves the layer ready for backward
     L.status()
+
+
+def test_protocol_assertions_single_gpu(monkeypatch):
+    """Debug mode on one GPU: the fused-dispatch arrival invariants hold for
+    CTA-pair and single-CTA tiles (moe_layer_status raises on a violation)."""
+    monkeypatch.setenv("MOE_DEBUG_CHECKS", "1")
+    for (T, h, f, E, k) in ((512, 512, 768, 8, 2), (512, 512, 256, 128, 8)):
+        L, x, *_ = make_layer(T, h, f, E, k, seed=31)
+        dy = (torch.randn(T, h) * 0.1).bfloat16().cuda()
+        for _ in range(2):
+            L.forward(x.cuda())
+            L.backward(dy)
+        L.status()

@@ -101,3 +101,13 @@ def test_ep4_full_shape_parity_deepseek_ag_rs():
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "MP_FULL_RESULT" in p.stdout
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("ep", ["a2a", "ag_rs"])
+def test_ep2_protocol_assertions(ep):
+    """MOE_DEBUG_CHECKS=1 (device-side protocol assertions in place of the
+    compute-sanitizer runs this pool does not allow): barrier epochs exact on
+    every slot, every dispatch block landed exactly once, dedup rows once,
+    all-gather chunks complete — over several steps, with drops and dedup."""
+    _run(2, {"MP_CF": "1.25", "MP_E": "8", "MP_K": "4", "MP_TR": "256", "MP_EP": ep, "MOE_DEBUG_CHECKS": "1"})
