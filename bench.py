@@ -896,11 +896,28 @@ def run_attn(args, cfg):
     launch_count_reset()
     step()
     per_step = launch_count()
+    nvl = None
+    if n > 1:
+        try:
+            nvl = NvlinkCounters(local)
+        except Exception:  # noqa: BLE001
+            nvl = None
+    nv0 = nvl.read() if nvl else None
     clocks = ClockSampler(local)
     clocks.start()
     ms = timed(step)
     clk = clocks.stop()
+    nv_step = None
+    if nvl:
+        nv1 = nvl.read()
+        nsteps = args.steps + args.warmup
+        nv_step = [(nv1[0] - nv0[0]) / nsteps, (nv1[1] - nv0[1]) / nsteps]
+    nv_all = None
+    if n > 1:
+        nv_all = [None] * n
+        dist.all_gather_object(nv_all, nv_step)
     ms_ag = timed(lambda: A.ag_gemm(None, qkv))
+    ms_rs_only = timed(lambda: A.gemm_rs(o, y))
     # NCCL + cuBLAS baseline for the same math
     xg = torch.empty(s_len, h, dtype=torch.bfloat16, device="cuda")
     part = torch.empty(s_len, h, dtype=torch.bfloat16, device="cuda")
@@ -934,7 +951,18 @@ def run_attn(args, cfg):
                          "target_ms": 1000 * max(t_tensor, t_link), "achieved_ms": ms,
                          "frac": 1000 * max(t_tensor, t_link) / ms,
                          "peak": "bf16 %.1f TF (measured burst), NVLink 770 GB/s/dir (measured ref.)" % peaks["bf16"]},
-            "ag_gemm_ms": ms_ag, "gemm_rs_ms": ms - ms_ag,
+            "ag_gemm_ms": ms_ag, "gemm_rs_ms": ms_rs_only,
+            "per_op_roofline": {
+                "ag_gemm": {"target_ms": 1000 * max(2.0 * s_len * h * nq / (peaks["bf16"] * 1e12),
+                                                    (n - 1) / n * s_len * h * 2 / 770e9 if n > 1 else 0.0),
+                            "achieved_ms": ms_ag},
+                "gemm_rs": {"target_ms": 1000 * max(2.0 * s_len * dh * h / (peaks["bf16"] * 1e12),
+                                                    (n - 1) / n * s_len * h * 2 / 770e9 if n > 1 else 0.0),
+                            "achieved_ms": ms_rs_only}},
+            "nvlink_measured_nvml": None if not nv_all or any(v is None for v in nv_all) else {
+                "tx_bytes_per_step_per_rank": [v[0] for v in nv_all], "rx_bytes_per_step_per_rank": [v[1] for v in nv_all],
+                "algorithmic_bytes_per_step_per_rank": 2.0 * (n - 1) / n * s_len * h * 2,
+                "GBps_rx_max": max(v[1] for v in nv_all) / (ms / 1000.0) / 1e9},
             "nccl_cublas_baseline_ms": ms_nccl, "speedup_vs_nccl_baseline": ms_nccl / ms,
             "clocks": clk, "gpu_launches": per_step * args.steps, "launch_mode": "eager",
             "e2e": None,
