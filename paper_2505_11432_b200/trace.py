@@ -101,6 +101,18 @@ def stamp_summary(all_ranks: list) -> dict:
             per_phase.setdefault(name, []).append(max(v))
         for name, v in busy.items():
             busy_phase.setdefault(name, []).append(max(v))
+    # per-rank busy time of the GEMM phases (median over steps): separates a
+    # slower GPU (clock / power) from routing imbalance
+    per_rank = {}
+    for r in all_ranks:
+        acc = {}
+        for s_ in range(nsteps):
+            st = r["steps"][s_]
+            wait_in = {BARRIER_PHASE[int(k_)]: (v_[1] - v_[0]) / 1e6 for k_, v_ in st["barriers"].items()}
+            for name, a, b in _intervals(st["phases"]):
+                acc.setdefault(name, []).append((b - a) / 1e6 - wait_in.get(name, 0.0))
+        per_rank[str(r["rank"])] = {k_: round(float(np.median(v_)), 4) for k_, v_ in acc.items()
+                                    if k_ in ("fc1", "fc2", "fc2_dgrad", "fc1_dgrad", "fc2_wgrad", "fc1_wgrad")}
     wait_med = {}
     for slot, lst in waits.items():
         by_step = {}
@@ -115,6 +127,7 @@ def stamp_summary(all_ranks: list) -> dict:
         "phases_busy_ms": {k: round(float(np.median(v)), 4) for k, v in busy_phase.items()},
         "barrier_wait_ms": {f"slot{k}_{BARRIER_PHASE[k]}": round(v, 4) for k, v in sorted(wait_med.items())},
         "rank_imbalance_idle_ms": round(sum(wait_med.values()), 4),
+        "per_rank_busy_gemm_ms": per_rank,
         "how": "device %globaltimer stamps at each phase boundary and at every flag barrier's entry/release, "
                "inside graph-replayed steps (each replay synchronised and read back); ranks aligned on the first "
                "barrier's release; phase = median over steps of the max over ranks; phases_busy = the same minus "
