@@ -141,8 +141,21 @@ moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_ran
     A->p_qkv.cg = A->cg;
     A->p_qkv.epi = EPI_STORE_BF16;
     A->p_qkv.dispatch = true;
+    {
+        // tile width by wave fit: at TP = 4 (N = 2560) 256 x 256 pair tiles make
+        // 320 tiles = 4.3 waves of 74 pairs (86% of the last wave idle-free),
+        // 256 x 128 tiles make 640 = 8.6 waves (96%)
+        auto eff = [&](int bn) {
+            const int64_t units = kNumSMs / A->cg;
+            const int64_t tiles = (A->s / (128 * A->cg)) * ((A->nq + bn - 1) / bn);
+            const int64_t waves = (tiles + units - 1) / units;
+            return double(tiles) / double(waves * units);
+        };
+        A->p_qkv.bn = (A->cg == 2 && A->nq % 128 == 0 && eff(128) > eff(256) + 0.05) ? 128 : 256;
+        if (const char* e = getenv("MOE_ATTN_QKV_BN")) A->p_qkv.bn = atoi(e) == 128 && A->cg == 2 ? 128 : 256;
+    }
     TRY(tmap_kmajor(&A->p_qkv.ta, A->x_all, A->s, A->h, 128));
-    TRY(tmap_kmajor(&A->p_qkv.tb, A->wqkv, A->nq, A->h, 256 / A->cg));
+    TRY(tmap_kmajor(&A->p_qkv.tb, A->wqkv, A->nq, A->h, A->p_qkv.bn / A->cg));
     A->p_qkv.counter = A->counters;
     A->p_out.cg = A->cg;
     A->p_out.epi = EPI_SCATTER;

@@ -95,6 +95,7 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     MOE_GEMM_CASE_DISP(256, 1, false, true, false, EPI_SWIGLU_BWD)
     MOE_GEMM_CASE_DISP(256, 2, false, false, false, EPI_STORE_BF16)  // attention AG-GEMM
     MOE_GEMM_CASE_DISP(256, 1, false, false, false, EPI_STORE_BF16)
+    MOE_GEMM_CASE_DISP(128, 2, false, false, false, EPI_STORE_BF16)  // AG-GEMM, 256 x 128 pair tiles
     // layer GEMMs, CTA-pair (cta_group::2) versions
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_SWIGLU)       // fc1 + SwiGLU
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_SCATTER)      // fc2 + gather
@@ -121,6 +122,8 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     MOE_GEMM_CASE(256, 1, false, false, false, EPI_STORE_F32)
     MOE_GEMM_CASE(256, 1, false, true, false, EPI_STORE_BF16)
     MOE_GEMM_CASE(256, 1, false, true, false, EPI_STORE_F32)
+    MOE_GEMM_CASE(128, 2, false, false, false, EPI_STORE_BF16)  // 256 x 128 pair tiles (wave fit)
+    MOE_GEMM_CASE(128, 2, false, false, false, EPI_STORE_F32)
     MOE_GEMM_CASE(128, 1, false, false, false, EPI_STORE_BF16)
     MOE_GEMM_CASE(128, 1, false, false, false, EPI_STORE_F32)
 #undef MOE_GEMM_CASE
@@ -178,7 +181,7 @@ extern "C" moe_status moe_grouped_gemm(const uint16_t* d_a, const uint16_t* d_b,
         MOE_TRY(tmap_kmajor(&p.ta, d_a, total_rows, K, 128));
         if (!b_mn_major) {
             a.b_group_stride = (int)N;
-            a.b_box_rows = b_box > 0 ? b_box : bn / p.cg;
+            a.b_box_rows = b_box > 0 ? b_box : bn / p.cg;   // = the CTA's B rows (256 / cg or 128 / cg)
             MOE_TRY(tmap_kmajor(&p.tb, d_b, (int64_t)groups * N, K, a.b_box_rows));
         } else {
             a.b_group_stride = (int)K;

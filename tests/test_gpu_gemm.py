@@ -20,10 +20,8 @@ def _rel(a, b):
 @pytest.mark.parametrize("cta_pair", [False, True])
 def test_m_grouped_kmajor(rows_per_group, N, K, bn, cta_pair):
     from paper_2505_11432_b200 import ops
-    if cta_pair:
-        if bn != 256:
-            pytest.skip("CTA pairs use 256-wide tiles")
-        # 128-row multiples: odd counts end in an M=128 pair tile
+    # cta_pair: 128-row multiples, odd counts end in an M=128 pair tile; bn = 128
+    # with pairs = 256 x 128 tiles (the attention AG-GEMM's wave-fit variant)
     torch.manual_seed(1)
     G = len(rows_per_group)
     rows = sum(rows_per_group)
