@@ -683,7 +683,7 @@ def run_ours(args, cfg):
         total_flops = 3.0 * rows_local * 6.0 * h * f  # fwd+bwd expert FFN
         traffic = None
         try:  # DRAM bytes per fc1 launch from the committed ncu capture (same workload)
-            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
                 if cfg["workload"].startswith("mixtral-8x7b-moe-layer-fwd+bwd") and n == 1:
                     traffic = json.load(fh)["kernels"]["fc1"]["traffic_bytes"]
         except Exception:

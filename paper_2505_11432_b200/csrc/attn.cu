@@ -143,15 +143,17 @@ moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_ran
     A->p_qkv.dispatch = true;
     {
         // tile width by wave fit: at TP = 4 (N = 2560) 256 x 256 pair tiles make
-        // 320 tiles = 4.3 waves of 74 pairs (86% of the last wave idle-free),
-        // 256 x 128 tiles make 640 = 8.6 waves (96%)
+        // 320 tiles = 4.3 waves of 74 pairs (86% busy), 256 x 128 tiles 640 = 8.6
+        // waves (96%) — but a 256 x 128 pair tile runs ~0.8x as fast per FLOP
+        // (measured at TP = 2: AG-GEMM 0.638 vs 0.512 ms), so 128 wins only when
+        // it fits the waves more than 1.25x better
         auto eff = [&](int bn) {
             const int64_t units = kNumSMs / A->cg;
             const int64_t tiles = (A->s / (128 * A->cg)) * ((A->nq + bn - 1) / bn);
             const int64_t waves = (tiles + units - 1) / units;
             return double(tiles) / double(waves * units);
         };
-        A->p_qkv.bn = (A->cg == 2 && A->nq % 128 == 0 && eff(128) > eff(256) + 0.05) ? 128 : 256;
+        A->p_qkv.bn = (A->cg == 2 && A->nq % 128 == 0 && 0.8 * eff(128) > eff(256)) ? 128 : 256;
         if (const char* e = getenv("MOE_ATTN_QKV_BN")) A->p_qkv.bn = atoi(e) == 128 && A->cg == 2 ? 128 : 256;
     }
     TRY(tmap_kmajor(&A->p_qkv.ta, A->x_all, A->s, A->h, 128));
