@@ -153,6 +153,14 @@ class NvlinkCounters:
             except Exception:
                 pass
 
+    def probe(self):
+        """True when the driver exposes the counters (NOT_SUPPORTED on some pools)."""
+        N = self.N
+        for link in self.links[:1]:
+            v = N.nvmlDeviceGetFieldValues(self.hd, [(self.TX, link)])[0]
+            return v.nvmlReturn == 0
+        return False
+
     def read(self):
         N = self.N
         tx = rx = 0
@@ -374,6 +382,8 @@ def run_ours(args, cfg):
     if world > 1:
         try:
             nvl = NvlinkCounters(local)
+            if not nvl.probe():
+                nvl = None
         except Exception:  # noqa: BLE001
             nvl = None
     nvl0 = nvl.read() if nvl else None
@@ -654,7 +664,25 @@ def run_ours(args, cfg):
                         "rx_bytes_per_step_per_rank": [m_[1] for m_ in allm],
                         "max_GBps_tx": tx_max / (ms / 1000.0) / 1e9, "max_GBps_rx": rx_max / (ms / 1000.0) / 1e9,
                         "frac_900_over_step": max(tx_max, rx_max) / (ms / 1000.0) / 900e9}
-        nvlink = {"measured_nvml": measured, "remote_rows": remote_rows, "remote_tokens": remote_tokens, "rows_pulled": pulled_fwd,
+        if measured is None:
+            measured = {"unavailable": "NVML NVLink throughput counters return NOT_SUPPORTED on this pool "
+                                       "(scripts/nvml_nvlink_probe.py); ncu NVLink metrics need one profiled "
+                                       "process per rank, which hangs the flag barriers"}
+        # the link rate each fused kernel needs: its NVLink bytes over its own busy
+        # time in the graph-replayed steps (max over ranks), against 900 GB/s
+        per_phase = None
+        busy = (gtrace or {}).get("summary", {}).get("phases_busy_ms") if isinstance(gtrace, dict) else None
+        if busy:
+            ph_bytes = {"fc1": pulled_fwd * h * bpe, "fc2": remote_rows * h * bpe,
+                        "fc2_dgrad": pulled_bwd * h * bpe, "fc1_dgrad": remote_rows * h * bpe}
+            if args.ep_pattern == "ag_rs":
+                ph_bytes = {"fc1": (n - 1) * Tr * h * bpe, "fc2": rs_rows * h * bpe,
+                            "fc2_dgrad": (n - 1) * Tr * h * bpe, "fc1_dgrad": rs_rows * h * bpe}
+            per_phase = {ph: {"bytes": b, "busy_ms": busy.get(ph),
+                              "GBps": (b / (busy[ph] / 1000.0) / 1e9) if busy.get(ph) else None,
+                              "frac_900": (b / (busy[ph] / 1000.0) / 900e9) if busy.get(ph) else None}
+                         for ph, b in ph_bytes.items()}
+        nvlink = {"measured_nvml": measured, "per_fused_kernel": per_phase, "remote_rows": remote_rows, "remote_tokens": remote_tokens, "rows_pulled": pulled_fwd,
                   "bytes_per_step": fwd_b + bwd_b,
                   "link_GBps_if_spread_over_step": (fwd_b + bwd_b) / (ms / 1000.0) / 1e9,
                   "link_time_ms_at_770GBps": (fwd_b + bwd_b) / 770e9 * 1000.0,
@@ -900,6 +928,8 @@ def run_attn(args, cfg):
     if n > 1:
         try:
             nvl = NvlinkCounters(local)
+            if not nvl.probe():
+                nvl = None
         except Exception:  # noqa: BLE001
             nvl = None
     nv0 = nvl.read() if nvl else None
