@@ -2,13 +2,23 @@
 // tokens, hidden 1024, ffn 2816, 8 experts top-2, fp32, checked against the
 // fp32 CPU oracle at 1e-5). Same operator chain as the bf16 path
 // (router -> capacity drop -> permutation -> dispatch -> fc1 -> SwiGLU (->
-// gate) -> fc2 -> gather -> combine, graph.cpp:254-311); the expert GEMMs run
-// as FFMA grouped GEMMs (128x128 tiles, 8x8 per thread, double-buffered
-// shared memory) because fp32 accuracy at 1e-5 rules out the tf32/bf16
-// tensor-core formats.
+// gate) -> fc2 -> gather -> combine, graph.cpp:254-311).
+//
+// Expert GEMMs: 3xTF32 on the tcgen05 tensor cores. Every fp32 operand x is
+// split into hi = tf32(x) (RN) and lo = x - hi (exact); A' = [A_hi | A_lo | A_hi]
+// and B' = [B_hi | B_hi | B_lo] concatenated along K make ONE grouped GEMM of
+// contraction 3K whose sum is A_hi.B_hi + A_lo.B_hi + A_hi.B_lo (the dropped
+// A_lo.B_lo term and the tf32 truncation of lo are ~2^-21 relative), i.e.
+// fp32-level accuracy at tensor-core speed. The same tcgen05 kernel as the bf16
+// layer runs it (kind::tf32: the fp32 bytes move through the identical TMA /
+// 128B-swizzle / descriptor pipeline, 32 bytes of K per MMA). MOE_F32_FFMA=1
+// selects the FFMA grouped GEMMs (128x128 tiles) instead, for A/B.
 #include <cmath>
 
+#include <cstdlib>
+
 #include "common.cuh"
+#include "gemm.h"
 #include "layer_kernels.cuh"
 #include "runtime.h"
 
@@ -138,6 +148,81 @@ __global__ void router_f32_kernel(const float* __restrict__ x, const float* __re
     }
 }
 
+// ---- 3xTF32 operand preparation ----
+__device__ __forceinline__ float tf32_rn(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+// dst row r = [hi | lo | hi] (A side, b_side = 0) or [hi | hi | lo] (B side)
+// of src row r; K multiple of 4.
+__global__ void split_tf32_rows_kernel(const float* __restrict__ src, int64_t rows, int K, int b_side,
+                                       float* __restrict__ dst) {
+    const int kv = K / 4;
+    const int64_t n = rows * kv;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / kv;
+        const int c = (int)(i - r * kv) * 4;
+        const float4 v = *reinterpret_cast<const float4*>(src + r * K + c);
+        const float4 hi = make_float4(tf32_rn(v.x), tf32_rn(v.y), tf32_rn(v.z), tf32_rn(v.w));
+        const float4 lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+        float* d = dst + r * 3 * K + c;
+        *reinterpret_cast<float4*>(d) = hi;
+        *reinterpret_cast<float4*>(d + K) = b_side ? hi : lo;
+        *reinterpret_cast<float4*>(d + 2 * K) = b_side ? lo : hi;
+    }
+}
+// dispatch + split: padded row pp = split(x[token of pp]) (A side), zeros for pads
+__global__ void gather_split_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad, int k,
+                                    const float* __restrict__ x, int h, float* __restrict__ dst) {
+    const int total = *nrows_pad;
+    const int hv = h / 4;
+    const int64_t n = (int64_t)total * hv;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pp = i / hv;
+        const int c = (int)(i - pp * hv) * 4;
+        const int tk = pad_row_tok[pp];
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (tk >= 0) v = *reinterpret_cast<const float4*>(x + (int64_t)(tk / k) * h + c);
+        const float4 hi = make_float4(tf32_rn(v.x), tf32_rn(v.y), tf32_rn(v.z), tf32_rn(v.w));
+        const float4 lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+        float* d = dst + pp * 3 * h + c;
+        *reinterpret_cast<float4*>(d) = hi;
+        *reinterpret_cast<float4*>(d + h) = lo;
+        *reinterpret_cast<float4*>(d + 2 * h) = hi;
+    }
+}
+// SwiGLU (+ gate) of fc1 rows, written split for the fc2 A operand
+__global__ void swiglu_split_kernel(const float* __restrict__ fc1, const float* __restrict__ row_gate,
+                                    const int32_t* nrows, int f, float* __restrict__ dst) {
+    const int64_t n = (int64_t)(*nrows) * f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / f, j = i - r * f;
+        const float a = fc1[r * 2 * f + j], b = fc1[r * 2 * f + f + j];
+        float v = a * (b / (1.0f + expf(-b)));
+        if (row_gate) v *= row_gate[r];
+        const float hi = tf32_rn(v);
+        float* d = dst + r * 3 * f + j;
+        d[0] = hi;
+        d[f] = v - hi;
+        d[2 * f] = hi;
+    }
+}
+// y[t] = sum over slots (fixed order) of the expert output rows of (t, slot)
+__global__ void combine_rows_f32_kernel(const float* __restrict__ rows, const int32_t* __restrict__ inv,
+                                        int T, int k, int h, float* __restrict__ y) {
+    const int64_t n = (int64_t)T * h;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / h, c = i - t * h;
+        float acc = 0.0f;
+        for (int j = 0; j < k; ++j) {
+            const int pp = inv[t * k + j];
+            if (pp >= 0) acc += rows[(int64_t)pp * h + c];
+        }
+        y[i] = acc;
+    }
+}
+
 __global__ void iota_src_kernel(int32_t* src, int T) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) src[t] = 0;
 }
@@ -211,6 +296,71 @@ extern "C" moe_status moe_ffn_forward_f32(const float* d_x, const float* d_w1, c
                            gpr, gpo, ptok, 128, s));
     row_info_kernel<<<(unsigned)E, 256, 0, s>>>(gpo, gpr, offs, ptok, d_gates, (int)k, (int)T, row_gate, rdst);
     count_launch();
+    const bool gate_after_ = gate_order == MOE_GATE_AFTER_FC2;
+    static const bool ffma = getenv("MOE_F32_FFMA") != nullptr;
+    if (!ffma && h % 32 == 0 && (2 * f) % 8 == 0) {
+        // ---- 3xTF32 tensor-core path ----
+        const int cg = double(T * k) / double(E) >= 256.0 ? 2 : 1;
+        float *xs = nullptr, *w1s = nullptr, *w2s = nullptr, *f2s = nullptr, *orow = nullptr;
+        int32_t* inv = nullptr;
+        MOE_TRY(salloc(&xs, Mp * 3 * h, s));
+        MOE_TRY(salloc(&w1s, E * 2 * f * 3 * h, s));
+        MOE_TRY(salloc(&w2s, E * h * 3 * f, s));
+        MOE_TRY(salloc(&f2s, Mp * 3 * f, s));
+        MOE_TRY(salloc(&orow, Mp * h, s));
+        MOE_TRY(salloc(&inv, T * k, s));
+        const int grid = kNumSMs * 8;
+        split_tf32_rows_kernel<<<grid, 256, 0, s>>>(d_w1, E * 2 * f, (int)h, 1, w1s);
+        split_tf32_rows_kernel<<<grid, 256, 0, s>>>(d_w2, E * h, (int)f, 1, w2s);
+        gather_split_kernel<<<grid, 256, 0, s>>>(ptok, gpo + E, (int)k, d_x, (int)h, xs);
+        count_launch(3);
+        // fc1: [Mp, 3h] x [E*2f, 3h]^T -> fc1 [Mp, 2f] fp32 (tensor maps over the fp32
+        // bytes as bf16 pairs: K counts 2-byte units)
+        GemmPlan p1;
+        p1.cg = cg;
+        p1.tf32 = true;
+        p1.epi = EPI_STORE_F32;
+        MOE_TRY(tmap_kmajor(&p1.ta, xs, Mp, 6 * h, 128));
+        MOE_TRY(tmap_kmajor(&p1.tb, w1s, E * 2 * f, 6 * h, 256 / cg));
+        GemmArgs a1{};
+        a1.G = (int)E;
+        a1.group_rows = gpr;
+        a1.N = (int)(2 * f);
+        a1.K = (int)(6 * h);
+        a1.b_group_stride = (int)(2 * f);
+        a1.out = fc1;
+        a1.ldo = 2 * f;
+        MOE_TRY(gemm_launch(p1, a1, s));
+        swiglu_split_kernel<<<grid, 256, 0, s>>>(fc1, gate_after_ ? nullptr : row_gate, gpo + E, (int)f, f2s);
+        count_launch();
+        GemmPlan p2;
+        p2.cg = cg;
+        p2.tf32 = true;
+        p2.epi = EPI_STORE_F32;
+        MOE_TRY(tmap_kmajor(&p2.ta, f2s, Mp, 6 * f, 128));
+        MOE_TRY(tmap_kmajor(&p2.tb, w2s, E * h, 6 * f, 256 / cg));
+        GemmArgs a2{};
+        a2.G = (int)E;
+        a2.group_rows = gpr;
+        a2.N = (int)h;
+        a2.K = (int)(6 * f);
+        a2.b_group_stride = (int)h;
+        a2.out = orow;
+        a2.ldo = h;
+        a2.row_gate = row_gate;
+        a2.gate_rows = gate_after_ ? 1 : 0;
+        MOE_TRY(gemm_launch(p2, a2, s));
+        MOE_CUDA_TRY(cudaMemsetAsync(inv, 0xff, T * k * 4, s));
+        inverse_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(ptok, gpo + E, inv);
+        combine_rows_f32_kernel<<<grid, 256, 0, s>>>(orow, inv, (int)T, (int)k, (int)h, d_y);
+        count_launch(2);
+        MOE_CUDA_TRY(cudaGetLastError());
+        void* bufs[] = {src, rmi, cnt, oe, osr, offs, rows, gpr, gpo, ptok, rdst, row_gate, x_perm, fc1, fc2_in,
+                        stage, ws, xs, w1s, w2s, f2s, orow, inv};
+        for (void* b : bufs) cudaFreeAsync(b, s);
+        if (own_logits) cudaFreeAsync(logits, s);
+        return MOE_OK;
+    }
     // dispatch: fp32 rows copied as 2x bf16-width rows (16-byte vector copy)
     const uint16_t* srcbuf = reinterpret_cast<const uint16_t*>(d_x);
     const uint16_t** tab = nullptr;

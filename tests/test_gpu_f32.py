@@ -1,7 +1,8 @@
 """BASELINE configs[0]: fp32 MoE layer forward (4096 tokens, hidden 1024,
 ffn 2816, 8 experts top-2) against the fp32 CPU oracle.
-Stated tolerance: relative L2 <= 1e-5 (FFMA fp32 accumulation vs the
-oracle's binary64 accumulation); routing bit-exact given the same logits."""
+Stated tolerance: relative L2 <= 1e-5 (3xTF32 tensor-core GEMMs with fp32
+accumulation, or the FFMA GEMMs with MOE_F32_FFMA=1, vs the oracle's binary64
+accumulation); routing bit-exact given the same logits."""
 import numpy as np
 import pytest
 import torch
@@ -61,3 +62,27 @@ def test_cfg1_fp32_injected_routing_with_golden_assignment():
     sample = np.arange(0, T, 5)
     oy = P.orc_moe_forward(x, ex, gates, np.zeros(T, np.uint8), w1, w2, tokens=sample)
     assert rel(y.cpu().numpy()[sample], oy) < 1e-5
+
+
+def test_cfg1_fp32_ffma_path_same_tolerance():
+    """The FFMA grouped-GEMM variant (MOE_F32_FFMA=1, read once per process) in a
+    subprocess: same layer, same tolerance."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import pyoracle as P\nfrom paper_2505_11432_b200 import ops\n"
+        "T,h,f,E,k=1024,1024,2816,8,2\nr=np.random.default_rng(3)\n"
+        "x=(r.standard_normal((T,h))*0.5).astype(np.float32)\n"
+        "w1=(r.standard_normal((E,2*f,h))/np.sqrt(h)).astype(np.float32)\n"
+        "w2=(r.standard_normal((E,h,f))/np.sqrt(f)).astype(np.float32)\n"
+        "wr=(r.standard_normal((E,h))/np.sqrt(h)).astype(np.float32)\n"
+        "y,ex,g,lg,dr=ops.ffn_forward_f32(*(torch.from_numpy(a).cuda() for a in (x,w1,w2,wr)),k)\n"
+        "s=np.arange(0,T,5)\noy=P.orc_moe_forward(x,ex.cpu().numpy(),g.cpu().numpy(),dr.cpu().numpy(),w1,w2,tokens=s)\n"
+        "e=np.linalg.norm(y.cpu().numpy()[s]-oy)/np.linalg.norm(oy)\nprint('ERR',e)\nassert e<1e-5\n"
+    ) % (root, os.path.join(root, "oracle"))
+    p = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, MOE_F32_FFMA="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
