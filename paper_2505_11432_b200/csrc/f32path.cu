@@ -4,15 +4,21 @@
 // (router -> capacity drop -> permutation -> dispatch -> fc1 -> SwiGLU (->
 // gate) -> fc2 -> gather -> combine, graph.cpp:254-311).
 //
-// Expert GEMMs: 3xTF32 on the tcgen05 tensor cores. Every fp32 operand x is
-// split into hi = tf32(x) (RN) and lo = x - hi (exact); A' = [A_hi | A_lo | A_hi]
-// and B' = [B_hi | B_hi | B_lo] concatenated along K make ONE grouped GEMM of
-// contraction 3K whose sum is A_hi.B_hi + A_lo.B_hi + A_hi.B_lo (the dropped
-// A_lo.B_lo term and the tf32 truncation of lo are ~2^-21 relative), i.e.
-// fp32-level accuracy at tensor-core speed. The same tcgen05 kernel as the bf16
-// layer runs it (kind::tf32: the fp32 bytes move through the identical TMA /
-// 128B-swizzle / descriptor pipeline, 32 bytes of K per MMA). MOE_F32_FFMA=1
-// selects the FFMA grouped GEMMs (128x128 tiles) instead, for A/B.
+// Expert GEMMs on the tcgen05 tensor cores with fp32 accuracy ("bf16x6"): every
+// fp32 operand x is split exactly into three bf16 pieces hi = bf16(x),
+// mid = bf16(x - hi), lo = bf16(x - hi - mid) (|x - hi - mid - lo| <= 2^-24 |x|).
+// With A' = [A_hi, A_hi, A_mid, A_hi, A_lo, A_mid] and B' = [B_hi, B_mid, B_hi,
+// B_lo, B_hi, B_mid] along K, A'.B'^T holds every cross term down to 2^-16
+// (hi.hi, hi.mid, mid.hi, hi.lo, lo.hi, mid.mid; the dropped ones are <= 2^-24)
+// and bf16 products are exact. Measured (scripts/probe_accum.py): the tcgen05
+// fp32 accumulator truncates at every MMA (all-positive data: -1.4e-5 relative
+// bias at K = 4096, -8.2e-5 at 16384, linear in K), so the error grows with the
+// number of MMAs adding into one accumulator. The hi.hi part (contraction K)
+// and the 2^-8-smaller corrections (5K) therefore run as two GEMMs over column
+// windows of the same split operands, summed in fp32 by the next kernel: the
+// truncation error stays that of a K-long accumulation (~1e-6 at these shapes)
+// instead of a 6K-long one (5.4e-5 measured in one pass). 6 bf16 MMAs cost what
+// 3 tf32 MMAs would. MOE_F32_FFMA=1 selects the FFMA grouped GEMMs, for A/B.
 #include <cmath>
 
 #include <cstdlib>
@@ -148,76 +154,74 @@ __global__ void router_f32_kernel(const float* __restrict__ x, const float* __re
     }
 }
 
-// ---- 3xTF32 operand preparation ----
-__device__ __forceinline__ float tf32_rn(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+// ---- bf16x6 operand preparation ----
+struct Bf3 { uint16_t hi, mid, lo; };
+__device__ __forceinline__ uint16_t bf16_bits(float v) {
+    __nv_bfloat16 b = __float2bfloat16_rn(v);
+    return *reinterpret_cast<uint16_t*>(&b);
 }
-// dst row r = [hi | lo | hi] (A side, b_side = 0) or [hi | hi | lo] (B side)
-// of src row r; K multiple of 4.
-__global__ void split_tf32_rows_kernel(const float* __restrict__ src, int64_t rows, int K, int b_side,
-                                       float* __restrict__ dst) {
-    const int kv = K / 4;
-    const int64_t n = rows * kv;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / kv;
-        const int c = (int)(i - r * kv) * 4;
-        const float4 v = *reinterpret_cast<const float4*>(src + r * K + c);
-        const float4 hi = make_float4(tf32_rn(v.x), tf32_rn(v.y), tf32_rn(v.z), tf32_rn(v.w));
-        const float4 lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
-        float* d = dst + r * 3 * K + c;
-        *reinterpret_cast<float4*>(d) = hi;
-        *reinterpret_cast<float4*>(d + K) = b_side ? hi : lo;
-        *reinterpret_cast<float4*>(d + 2 * K) = b_side ? lo : hi;
+__device__ __forceinline__ float bf16_val(uint16_t u) { return __uint_as_float((uint32_t)u << 16); }
+__device__ __forceinline__ Bf3 split3(float x) {
+    Bf3 r;
+    r.hi = bf16_bits(x);
+    const float r1 = x - bf16_val(r.hi);     // exact
+    r.mid = bf16_bits(r1);
+    const float r2 = r1 - bf16_val(r.mid);   // exact
+    r.lo = bf16_bits(r2);
+    return r;
+}
+// piece order along K: A side [hi, hi, mid, hi, lo, mid], B side [hi, mid, hi, lo, hi, mid]
+__device__ __forceinline__ void store6(uint16_t* d, int64_t K, const Bf3& v, int b_side) {
+    if (!b_side) {
+        d[0] = v.hi; d[K] = v.hi; d[2 * K] = v.mid; d[3 * K] = v.hi; d[4 * K] = v.lo; d[5 * K] = v.mid;
+    } else {
+        d[0] = v.hi; d[K] = v.mid; d[2 * K] = v.hi; d[3 * K] = v.lo; d[4 * K] = v.hi; d[5 * K] = v.mid;
     }
 }
-// dispatch + split: padded row pp = split(x[token of pp]) (A side), zeros for pads
-__global__ void gather_split_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad, int k,
-                                    const float* __restrict__ x, int h, float* __restrict__ dst) {
-    const int total = *nrows_pad;
-    const int hv = h / 4;
-    const int64_t n = (int64_t)total * hv;
+// dst row r [6K] (bf16) = the pieces of src row r [K] (fp32)
+__global__ void split6_rows_kernel(const float* __restrict__ src, int64_t rows, int K, int b_side,
+                                   uint16_t* __restrict__ dst) {
+    const int64_t n = rows * K;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t pp = i / hv;
-        const int c = (int)(i - pp * hv) * 4;
+        const int64_t r = i / K, c = i - r * K;
+        store6(dst + r * 6 * K + c, K, split3(src[i]), b_side);
+    }
+}
+// dispatch + split: padded row pp = pieces of x[token of pp] (A side), zeros for pads
+__global__ void gather_split6_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad, int k,
+                                     const float* __restrict__ x, int h, uint16_t* __restrict__ dst) {
+    const int64_t n = (int64_t)(*nrows_pad) * h;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pp = i / h, c = i - pp * h;
         const int tk = pad_row_tok[pp];
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (tk >= 0) v = *reinterpret_cast<const float4*>(x + (int64_t)(tk / k) * h + c);
-        const float4 hi = make_float4(tf32_rn(v.x), tf32_rn(v.y), tf32_rn(v.z), tf32_rn(v.w));
-        const float4 lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
-        float* d = dst + pp * 3 * h + c;
-        *reinterpret_cast<float4*>(d) = hi;
-        *reinterpret_cast<float4*>(d + h) = lo;
-        *reinterpret_cast<float4*>(d + 2 * h) = hi;
+        const float v = tk >= 0 ? x[(int64_t)(tk / k) * h + c] : 0.0f;
+        store6(dst + pp * 6 * h + c, h, split3(v), 0);
     }
 }
-// SwiGLU (+ gate) of fc1 rows, written split for the fc2 A operand
-__global__ void swiglu_split_kernel(const float* __restrict__ fc1, const float* __restrict__ row_gate,
-                                    const int32_t* nrows, int f, float* __restrict__ dst) {
+// SwiGLU (+ gate) of fc1 rows, written as fc2 A-side pieces
+__global__ void swiglu_split6_kernel(const float* __restrict__ fc1, const float* __restrict__ fc1c,
+                                     const float* __restrict__ row_gate, const int32_t* nrows, int f,
+                                     uint16_t* __restrict__ dst) {
     const int64_t n = (int64_t)(*nrows) * f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = i / f, j = i - r * f;
-        const float a = fc1[r * 2 * f + j], b = fc1[r * 2 * f + f + j];
+        const float a = fc1[r * 2 * f + j] + fc1c[r * 2 * f + j];
+        const float b = fc1[r * 2 * f + f + j] + fc1c[r * 2 * f + f + j];
         float v = a * (b / (1.0f + expf(-b)));
         if (row_gate) v *= row_gate[r];
-        const float hi = tf32_rn(v);
-        float* d = dst + r * 3 * f + j;
-        d[0] = hi;
-        d[f] = v - hi;
-        d[2 * f] = hi;
+        store6(dst + r * 6 * f + j, f, split3(v), 0);
     }
 }
 // y[t] = sum over slots (fixed order) of the expert output rows of (t, slot)
-__global__ void combine_rows_f32_kernel(const float* __restrict__ rows, const int32_t* __restrict__ inv,
-                                        int T, int k, int h, float* __restrict__ y) {
+__global__ void combine_rows_f32_kernel(const float* __restrict__ rows, const float* __restrict__ rows_c,
+                                        const int32_t* __restrict__ inv, int T, int k, int h, float* __restrict__ y) {
     const int64_t n = (int64_t)T * h;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = i / h, c = i - t * h;
         float acc = 0.0f;
         for (int j = 0; j < k; ++j) {
             const int pp = inv[t * k + j];
-            if (pp >= 0) acc += rows[(int64_t)pp * h + c];
+            if (pp >= 0) acc += rows[(int64_t)pp * h + c] + rows_c[(int64_t)pp * h + c];
         }
         y[i] = acc;
     }
@@ -249,6 +253,23 @@ extern "C" moe_status moe_ffn_forward_f32(const float* d_x, const float* d_w1, c
                   "need h % 8 == 0, f % 4 == 0, 1 <= k <= min(8, E)");
     MOE_CHECK_ARG(d_experts_in || d_wr, "need a router weight or injected routing");
     cudaStream_t s = (cudaStream_t)stream;
+    {
+        // the per-call work buffers come from the device's stream-ordered pool;
+        // keep freed blocks in the pool (default threshold 0 returns them to the
+        // driver at every synchronisation, and re-mapping ~2 GB per call costs
+        // more than the layer itself)
+        int dev = 0;
+        cudaGetDevice(&dev);
+        static uint64_t pool_done = 0;
+        if (!(pool_done >> (dev & 63) & 1)) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            pool_done |= 1ull << (dev & 63);
+        }
+    }
     const int64_t Mp = T * k + E * 128;
     float *logits = d_logits, *x_perm = nullptr, *fc1 = nullptr, *fc2_in = nullptr, *stage = nullptr,
           *row_gate = nullptr;
@@ -298,65 +319,79 @@ extern "C" moe_status moe_ffn_forward_f32(const float* d_x, const float* d_w1, c
     count_launch();
     const bool gate_after_ = gate_order == MOE_GATE_AFTER_FC2;
     static const bool ffma = getenv("MOE_F32_FFMA") != nullptr;
-    if (!ffma && h % 32 == 0 && (2 * f) % 8 == 0) {
-        // ---- 3xTF32 tensor-core path ----
+    if (!ffma && h % 64 == 0 && f % 64 == 0) {
+        // ---- bf16x6 tensor-core path ----
         const int cg = double(T * k) / double(E) >= 256.0 ? 2 : 1;
-        float *xs = nullptr, *w1s = nullptr, *w2s = nullptr, *f2s = nullptr, *orow = nullptr;
+        uint16_t *xs = nullptr, *w1s = nullptr, *w2s = nullptr, *f2s = nullptr;
+        float* orow = nullptr;
         int32_t* inv = nullptr;
-        MOE_TRY(salloc(&xs, Mp * 3 * h, s));
-        MOE_TRY(salloc(&w1s, E * 2 * f * 3 * h, s));
-        MOE_TRY(salloc(&w2s, E * h * 3 * f, s));
-        MOE_TRY(salloc(&f2s, Mp * 3 * f, s));
+        MOE_TRY(salloc(&xs, Mp * 6 * h, s));
+        MOE_TRY(salloc(&w1s, E * 2 * f * 6 * h, s));
+        MOE_TRY(salloc(&w2s, E * h * 6 * f, s));
+        MOE_TRY(salloc(&f2s, Mp * 6 * f, s));
         MOE_TRY(salloc(&orow, Mp * h, s));
         MOE_TRY(salloc(&inv, T * k, s));
         const int grid = kNumSMs * 8;
-        split_tf32_rows_kernel<<<grid, 256, 0, s>>>(d_w1, E * 2 * f, (int)h, 1, w1s);
-        split_tf32_rows_kernel<<<grid, 256, 0, s>>>(d_w2, E * h, (int)f, 1, w2s);
-        gather_split_kernel<<<grid, 256, 0, s>>>(ptok, gpo + E, (int)k, d_x, (int)h, xs);
+        split6_rows_kernel<<<grid, 256, 0, s>>>(d_w1, E * 2 * f, (int)h, 1, w1s);
+        split6_rows_kernel<<<grid, 256, 0, s>>>(d_w2, E * h, (int)f, 1, w2s);
+        gather_split6_kernel<<<grid, 256, 0, s>>>(ptok, gpo + E, (int)k, d_x, (int)h, xs);
         count_launch(3);
-        // fc1: [Mp, 3h] x [E*2f, 3h]^T -> fc1 [Mp, 2f] fp32 (tensor maps over the fp32
-        // bytes as bf16 pairs: K counts 2-byte units)
-        GemmPlan p1;
-        p1.cg = cg;
-        p1.tf32 = true;
-        p1.epi = EPI_STORE_F32;
-        MOE_TRY(tmap_kmajor(&p1.ta, xs, Mp, 6 * h, 128));
-        MOE_TRY(tmap_kmajor(&p1.tb, w1s, E * 2 * f, 6 * h, 256 / cg));
-        GemmArgs a1{};
-        a1.G = (int)E;
-        a1.group_rows = gpr;
-        a1.N = (int)(2 * f);
-        a1.K = (int)(6 * h);
-        a1.b_group_stride = (int)(2 * f);
-        a1.out = fc1;
-        a1.ldo = 2 * f;
-        MOE_TRY(gemm_launch(p1, a1, s));
-        swiglu_split_kernel<<<grid, 256, 0, s>>>(fc1, gate_after_ ? nullptr : row_gate, gpo + E, (int)f, f2s);
+        // two GEMMs over column windows of the split operands (row stride 6K):
+        // main = hi.hi (K columns), corr = the five correction blocks (5K columns)
+        auto window = [](CUtensorMap* m, const uint16_t* base, int64_t rows, int64_t Kp, int64_t first,
+                         int64_t width, int box_rows) {
+            return make_tmap_2d(m, base + first, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)width,
+                                (uint64_t)rows, (uint64_t)(6 * Kp * 2), 64, (uint32_t)box_rows);
+        };
+        float* fc1c = nullptr;
+        float* orowc = nullptr;
+        MOE_TRY(salloc(&fc1c, Mp * 2 * f, s));
+        MOE_TRY(salloc(&orowc, Mp * h, s));
+        for (int part = 0; part < 2; ++part) {
+            const int64_t first = part ? h : 0, width = part ? 5 * h : h;
+            GemmPlan p1;
+            p1.cg = cg;
+            p1.epi = EPI_STORE_F32;
+            MOE_TRY(window(&p1.ta, xs, Mp, h, first, width, 128));
+            MOE_TRY(window(&p1.tb, w1s, E * 2 * f, h, first, width, 256 / cg));
+            GemmArgs a1{};
+            a1.G = (int)E;
+            a1.group_rows = gpr;
+            a1.N = (int)(2 * f);
+            a1.K = (int)width;
+            a1.b_group_stride = (int)(2 * f);
+            a1.out = part ? fc1c : fc1;
+            a1.ldo = 2 * f;
+            MOE_TRY(gemm_launch(p1, a1, s));
+        }
+        swiglu_split6_kernel<<<grid, 256, 0, s>>>(fc1, fc1c, gate_after_ ? nullptr : row_gate, gpo + E, (int)f, f2s);
         count_launch();
-        GemmPlan p2;
-        p2.cg = cg;
-        p2.tf32 = true;
-        p2.epi = EPI_STORE_F32;
-        MOE_TRY(tmap_kmajor(&p2.ta, f2s, Mp, 6 * f, 128));
-        MOE_TRY(tmap_kmajor(&p2.tb, w2s, E * h, 6 * f, 256 / cg));
-        GemmArgs a2{};
-        a2.G = (int)E;
-        a2.group_rows = gpr;
-        a2.N = (int)h;
-        a2.K = (int)(6 * f);
-        a2.b_group_stride = (int)h;
-        a2.out = orow;
-        a2.ldo = h;
-        a2.row_gate = row_gate;
-        a2.gate_rows = gate_after_ ? 1 : 0;
-        MOE_TRY(gemm_launch(p2, a2, s));
+        for (int part = 0; part < 2; ++part) {
+            const int64_t first = part ? f : 0, width = part ? 5 * f : f;
+            GemmPlan p2;
+            p2.cg = cg;
+            p2.epi = EPI_STORE_F32;
+            MOE_TRY(window(&p2.ta, f2s, Mp, f, first, width, 128));
+            MOE_TRY(window(&p2.tb, w2s, E * h, f, first, width, 256 / cg));
+            GemmArgs a2{};
+            a2.G = (int)E;
+            a2.group_rows = gpr;
+            a2.N = (int)h;
+            a2.K = (int)width;
+            a2.b_group_stride = (int)h;
+            a2.out = part ? orowc : orow;
+            a2.ldo = h;
+            a2.row_gate = row_gate;
+            a2.gate_rows = gate_after_ ? 1 : 0;
+            MOE_TRY(gemm_launch(p2, a2, s));
+        }
         MOE_CUDA_TRY(cudaMemsetAsync(inv, 0xff, T * k * 4, s));
         inverse_rows_kernel<<<kNumSMs * 2, 256, 0, s>>>(ptok, gpo + E, inv);
-        combine_rows_f32_kernel<<<grid, 256, 0, s>>>(orow, inv, (int)T, (int)k, (int)h, d_y);
+        combine_rows_f32_kernel<<<grid, 256, 0, s>>>(orow, orowc, inv, (int)T, (int)k, (int)h, d_y);
         count_launch(2);
         MOE_CUDA_TRY(cudaGetLastError());
         void* bufs[] = {src, rmi, cnt, oe, osr, offs, rows, gpr, gpo, ptok, rdst, row_gate, x_perm, fc1, fc2_in,
-                        stage, ws, xs, w1s, w2s, f2s, orow, inv};
+                        stage, ws, xs, w1s, w2s, f2s, orow, inv, fc1c, orowc};
         for (void* b : bufs) cudaFreeAsync(b, s);
         if (own_logits) cudaFreeAsync(logits, s);
         return MOE_OK;

@@ -28,11 +28,11 @@ static int* tile_counter_slot(int dev) {
     return base[dev] + (next[dev].fetch_add(1) % kCounters);
 }
 
-template <int BN, int CG, bool A_MN, bool B_MN, bool KG, int EPI, bool DISP = false, bool TF32 = false>
+template <int BN, int CG, bool A_MN, bool B_MN, bool KG, int EPI, bool DISP = false>
 static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
                               int grid, cudaStream_t s) {
     using Cfg = GemmCfg<BN, CG>;
-    auto kern = grouped_gemm_kernel<BN, CG, A_MN, B_MN, KG, EPI, DISP, TF32>;
+    auto kern = grouped_gemm_kernel<BN, CG, A_MN, B_MN, KG, EPI, DISP>;
     constexpr int kThreads = Cfg::THREADS + (DISP ? 32 * Cfg::COMM_WARPS : 0);
     static uint64_t attr_set = 0;  // per instantiation, one bit per device
     int dev = 0;
@@ -82,20 +82,13 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     }
 #define MOE_GEMM_CASE(BN, CG, AMN, BMN, KG, EPI)                                              \
     if (p.bn == BN && p.cg == CG && p.a_mn == AMN && p.b_mn == BMN && p.k_grouped == KG &&   \
-        p.epi == EPI && !p.dispatch && !p.tf32)                                               \
+        p.epi == EPI && !p.dispatch)                                                          \
         return launch_impl<BN, CG, AMN, BMN, KG, EPI>(p.ta, p.tb, a, grid, s);
-#define MOE_GEMM_CASE_TF32(BN, CG, EPI)                                                       \
-    if (p.bn == BN && p.cg == CG && !p.a_mn && !p.b_mn && !p.k_grouped && p.epi == EPI &&    \
-        !p.dispatch && p.tf32)                                                                \
-        return launch_impl<BN, CG, false, false, false, EPI, false, true>(p.ta, p.tb, a, grid, s);
 #define MOE_GEMM_CASE_DISP(BN, CG, AMN, BMN, KG, EPI)                                         \
     if (p.bn == BN && p.cg == CG && p.a_mn == AMN && p.b_mn == BMN && p.k_grouped == KG &&   \
-        p.epi == EPI && p.dispatch && !p.tf32)                                                \
+        p.epi == EPI && p.dispatch)                                                           \
         return launch_impl<BN, CG, AMN, BMN, KG, EPI, true>(p.ta, p.tb, a, grid, s);
     // fused AG + scatter + GroupedGEMM (fc1 forward, fc2 dgrad)
-    // 3xTF32 fp32 layer (configs[0]): K-major fp32 operands, fp32 rows out
-    MOE_GEMM_CASE_TF32(256, 2, EPI_STORE_F32)
-    MOE_GEMM_CASE_TF32(256, 1, EPI_STORE_F32)
     MOE_GEMM_CASE_DISP(256, 2, false, false, false, EPI_SWIGLU)
     MOE_GEMM_CASE_DISP(256, 2, false, true, false, EPI_SWIGLU_BWD)
     MOE_GEMM_CASE_DISP(256, 1, false, false, false, EPI_SWIGLU)
@@ -134,7 +127,6 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     MOE_GEMM_CASE(128, 1, false, false, false, EPI_STORE_BF16)
     MOE_GEMM_CASE(128, 1, false, false, false, EPI_STORE_F32)
 #undef MOE_GEMM_CASE
-#undef MOE_GEMM_CASE_TF32
 #undef MOE_GEMM_CASE_DISP
     return set_error(MOE_ERR_UNSUPPORTED,
                      "grouped GEMM variant not instantiated (bn=%d cg=%d a_mn=%d b_mn=%d kg=%d epi=%d)",

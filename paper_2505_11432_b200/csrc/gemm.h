@@ -13,8 +13,6 @@ struct GemmPlan {
     bool a_mn = false, b_mn = false, k_grouped = false;
     int epi = EPI_STORE_BF16;
     bool dispatch = false;  // fused AG + scatter of the A operand
-    bool tf32 = false;      // fp32 operands through kind::tf32 (tensor maps over the fp32 bytes as
-                            // bf16 pairs: K counts bf16-sized units, 64 per 128-byte k-block)
     int grid = 0;  // 0 = one CTA per SM
     // dynamic-schedule tile counter owned by the plan's object (layer, attn,
     // ulysses), so a CUDA graph that captured it never shares it with a later

@@ -279,37 +279,6 @@ __device__ __forceinline__ void umma_bf16_warp(uint32_t tmem_d, uint64_t adesc, 
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
-__device__ __forceinline__ void umma_tf32_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                              uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// kind::tf32 (K = 8 per instruction = 32 bytes, the same smem byte layout and
-// descriptor steps as bf16 with K = 16): the fp32 operands of the 3xTF32 path
-__device__ __forceinline__ void umma_tf32_2sm_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                                   uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void umma_tf32_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                               uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
 __device__ __forceinline__ void umma_commit_2sm_mc_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .b16 m;\n\t.reg .pred e;\n\tmov.b16 m, 3;\n\t"
@@ -791,7 +760,7 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int lane
     }
 }
 
-template <int BN, int CG, bool A_MN, bool B_MN, bool K_GROUPED, int EPI, bool DISPATCH = false, bool TF32 = false>
+template <int BN, int CG, bool A_MN, bool B_MN, bool K_GROUPED, int EPI, bool DISPATCH = false>
 __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * GemmCfg<BN, CG>::COMM_WARPS : 0), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
@@ -1055,10 +1024,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
         // and one elected lane issues: no per-MMA register broadcast loops.
         auto mma_role = [&](auto conv_tag) {
             constexpr bool CONV = decltype(conv_tag)::value;
-            // operand format: 1 = bf16 (kind::f16), 2 = tf32 (kind::tf32)
-            constexpr uint32_t kFmt = TF32 ? 2u : 1u;
-            constexpr uint32_t idesc_full = make_idesc(TILE_M, BN, kFmt, A_MN, B_MN);
-            constexpr uint32_t idesc_half = make_idesc(128, BN, kFmt, A_MN, B_MN);
+            constexpr uint32_t idesc_full = make_idesc(TILE_M, BN, 1, A_MN, B_MN);
+            constexpr uint32_t idesc_half = make_idesc(128, BN, 1, A_MN, B_MN);
             // stage s's descriptors = stage 0's + s * STAGE_BYTES / 16 (14-bit
             // address field, smem < 256 KB); k step within a stage: +32 B
             // (K-major) or +2048 B (MN-major), i.e. +2 / +128 in 16-byte units
@@ -1089,16 +1056,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t ad = ad0 + kk * a_kstep, bd = bd0 + kk * b_kstep;
-                        if constexpr (TF32) {
-                            // fp32 bytes through the bf16 pipeline: one tf32 MMA per 32 B of K
-                            if (CONV) {
-                                if (CG == 2) umma_tf32_2sm_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-                                else umma_tf32_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-                            } else {
-                                if (CG == 2) umma_tf32_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-                                else umma_tf32(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-                            }
-                        } else if (CONV) {
+                        if (CONV) {
                             if (CG == 2) umma_bf16_2sm_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                             else umma_bf16_warp(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                         } else {

@@ -1,8 +1,9 @@
 """BASELINE configs[0]: fp32 MoE layer forward (4096 tokens, hidden 1024,
 ffn 2816, 8 experts top-2) against the fp32 CPU oracle.
-Stated tolerance: relative L2 <= 1e-5 (3xTF32 tensor-core GEMMs with fp32
-accumulation, or the FFMA GEMMs with MOE_F32_FFMA=1, vs the oracle's binary64
-accumulation); routing bit-exact given the same logits."""
+Stated tolerance: relative L2 <= 1e-5 (bf16x6 tensor-core GEMMs: exact bf16
+products of the three-piece split, fp32 accumulation; or the FFMA GEMMs with
+MOE_F32_FFMA=1; vs the oracle's binary64 accumulation); routing bit-exact given
+the same logits."""
 import numpy as np
 import pytest
 import torch
