@@ -170,46 +170,75 @@ __device__ __forceinline__ Bf3 split3(float x) {
     r.lo = bf16_bits(r2);
     return r;
 }
-// piece order along K: A side [hi, hi, mid, hi, lo, mid], B side [hi, mid, hi, lo, hi, mid]
-__device__ __forceinline__ void store6(uint16_t* d, int64_t K, const Bf3& v, int b_side) {
-    if (!b_side) {
-        d[0] = v.hi; d[K] = v.hi; d[2 * K] = v.mid; d[3 * K] = v.hi; d[4 * K] = v.lo; d[5 * K] = v.mid;
-    } else {
-        d[0] = v.hi; d[K] = v.mid; d[2 * K] = v.hi; d[3 * K] = v.lo; d[4 * K] = v.hi; d[5 * K] = v.mid;
+// piece order along K: A side [hi, hi, mid, hi, lo, mid], B side [hi, mid, hi, lo, hi, mid].
+// 8 consecutive elements per thread: one 16-byte store per piece.
+__device__ __forceinline__ void store6x8(uint16_t* d, int64_t K, const float (&v)[8], int b_side) {
+    uint32_t hi[4], mid[4], lo[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const Bf3 a = split3(v[2 * q]), b = split3(v[2 * q + 1]);
+        hi[q] = (uint32_t)a.hi | ((uint32_t)b.hi << 16);
+        mid[q] = (uint32_t)a.mid | ((uint32_t)b.mid << 16);
+        lo[q] = (uint32_t)a.lo | ((uint32_t)b.lo << 16);
     }
+    const uint4 H = make_uint4(hi[0], hi[1], hi[2], hi[3]), M = make_uint4(mid[0], mid[1], mid[2], mid[3]),
+                Lo = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    const uint4 seq_a[6] = {H, H, M, H, Lo, M}, seq_b[6] = {H, M, H, Lo, H, M};
+#pragma unroll
+    for (int j = 0; j < 6; ++j) *reinterpret_cast<uint4*>(d + j * K) = b_side ? seq_b[j] : seq_a[j];
 }
-// dst row r [6K] (bf16) = the pieces of src row r [K] (fp32)
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+    const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+// dst row r [6K] (bf16) = the pieces of src row r [K] (fp32); K % 8 == 0
 __global__ void split6_rows_kernel(const float* __restrict__ src, int64_t rows, int K, int b_side,
                                    uint16_t* __restrict__ dst) {
-    const int64_t n = rows * K;
+    const int kv = K / 8;
+    const int64_t n = rows * kv;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / K, c = i - r * K;
-        store6(dst + r * 6 * K + c, K, split3(src[i]), b_side);
+        const int64_t r = i / kv;
+        const int c = (int)(i - r * kv) * 8;
+        float v[8];
+        load8(src + r * K + c, v);
+        store6x8(dst + r * 6 * K + c, K, v, b_side);
     }
 }
 // dispatch + split: padded row pp = pieces of x[token of pp] (A side), zeros for pads
 __global__ void gather_split6_kernel(const int32_t* __restrict__ pad_row_tok, const int32_t* nrows_pad, int k,
                                      const float* __restrict__ x, int h, uint16_t* __restrict__ dst) {
-    const int64_t n = (int64_t)(*nrows_pad) * h;
+    const int hv = h / 8;
+    const int64_t n = (int64_t)(*nrows_pad) * hv;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t pp = i / h, c = i - pp * h;
+        const int64_t pp = i / hv;
+        const int c = (int)(i - pp * hv) * 8;
         const int tk = pad_row_tok[pp];
-        const float v = tk >= 0 ? x[(int64_t)(tk / k) * h + c] : 0.0f;
-        store6(dst + pp * 6 * h + c, h, split3(v), 0);
+        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (tk >= 0) load8(x + (int64_t)(tk / k) * h + c, v);
+        store6x8(dst + pp * 6 * h + c, h, v, 0);
     }
 }
-// SwiGLU (+ gate) of fc1 rows, written as fc2 A-side pieces
+// SwiGLU (+ gate) of fc1 rows (main + correction GEMM outputs), written as fc2 A-side pieces
 __global__ void swiglu_split6_kernel(const float* __restrict__ fc1, const float* __restrict__ fc1c,
                                      const float* __restrict__ row_gate, const int32_t* nrows, int f,
                                      uint16_t* __restrict__ dst) {
-    const int64_t n = (int64_t)(*nrows) * f;
+    const int fv = f / 8;
+    const int64_t n = (int64_t)(*nrows) * fv;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / f, j = i - r * f;
-        const float a = fc1[r * 2 * f + j] + fc1c[r * 2 * f + j];
-        const float b = fc1[r * 2 * f + f + j] + fc1c[r * 2 * f + f + j];
-        float v = a * (b / (1.0f + expf(-b)));
-        if (row_gate) v *= row_gate[r];
-        store6(dst + r * 6 * f + j, f, split3(v), 0);
+        const int64_t r = i / fv;
+        const int j = (int)(i - r * fv) * 8;
+        float a[8], ac[8], b[8], bc[8], v[8];
+        load8(fc1 + r * 2 * f + j, a);
+        load8(fc1c + r * 2 * f + j, ac);
+        load8(fc1 + r * 2 * f + f + j, b);
+        load8(fc1c + r * 2 * f + f + j, bc);
+        const float g = row_gate ? row_gate[r] : 1.0f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float av = a[q] + ac[q], bv = b[q] + bc[q];
+            v[q] = av * (bv / (1.0f + expf(-bv))) * g;
+        }
+        store6x8(dst + r * 6 * f + j, f, v, 0);
     }
 }
 // y[t] = sum over slots (fixed order) of the expert output rows of (t, slot)

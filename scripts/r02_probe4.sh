@@ -1,5 +1,5 @@
 #!/bin/bash
-O=gpurun_out/r02w
+O=gpurun_out/r02x
 mkdir -p $O
 timeout 300 python scripts/probe_f32.py err > $O/err_bf16x6.log 2>&1
 timeout 300 python scripts/probe_accum.py > $O/accum.log 2>&1
