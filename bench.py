@@ -504,30 +504,41 @@ def run_ours(args, cfg):
             from paper_2505_11432_b200.trace import stamp_summary
             gtrace = stamp_summary(allst)
 
-    # ---- NCCL all-to-all + cuBLAS baseline (standard unfused EP), same shapes ----
+    # ---- NCCL all-to-all baselines (standard unfused EP), same shapes ----
     nccl_ms = None
+    nccl_gm_ms = None
     if not args.no_nccl_baseline and not injected and cfg.get("comm", "bf16") == "bf16":
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
-        from nccl_moe_baseline import NcclMoEBaseline
+        from nccl_moe_baseline import NcclMoEBaseline, NcclMoEGroupedBaseline
         g2 = torch.Generator(device="cuda").manual_seed(42)
         bw1 = (torch.randn(el, 2 * f, h, device="cuda", generator=g2) / h ** 0.5).bfloat16()
         bw2 = (torch.randn(el, h, f, device="cuda", generator=g2) / f ** 0.5).bfloat16()
-        base = NcclMoEBaseline(Tr, h, f, E, k, n, rank, bw1, bw2, wr)
-        for _ in range(2):
-            base.step(x, dy)
-        sync_all()
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        nb = max(3, args.steps // 5)
-        b0.record(stream)
-        for _ in range(nb):
-            base.step(x, dy)
-        b1.record(stream)
-        sync_all()
-        tb = torch.tensor([b0.elapsed_time(b1) / nb], device="cuda")
-        if world > 1:
-            dist.all_reduce(tb, op=dist.ReduceOp.MAX)
-        nccl_ms = float(tb.item())
-        del base, bw1, bw2
+
+        def time_baseline(cls):
+            base = cls(Tr, h, f, E, k, n, rank, bw1, bw2, wr)
+            for _ in range(2):
+                base.step(x, dy)
+            sync_all()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nb = max(3, args.steps // 5)
+            b0.record(stream)
+            for _ in range(nb):
+                base.step(x, dy)
+            b1.record(stream)
+            sync_all()
+            tb = torch.tensor([b0.elapsed_time(b1) / nb], device="cuda")
+            if world > 1:
+                dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+            del base
+            torch.cuda.empty_cache()
+            return float(tb.item())
+        nccl_ms = time_baseline(NcclMoEBaseline)
+        try:
+            nccl_gm_ms = time_baseline(NcclMoEGroupedBaseline)
+        except Exception as e:  # noqa: BLE001
+            nccl_gm_ms = None
+            print("grouped_mm baseline failed:", str(e)[:200], file=sys.stderr)
+        del bw1, bw2
         torch.cuda.empty_cache()
 
     # ---- per-phase device times (one instrumented step, same stream) ----
@@ -768,6 +779,11 @@ def run_ours(args, cfg):
                 "ms_per_step": nccl_ms, "tokens_per_s": n * Tr / (nccl_ms / 1000.0),
                 "speedup_of_fused": nccl_ms / ms,
                 "what": "standard EP: NCCL all_to_all_single dispatch/combine + per-expert cuBLAS (torch) fwd+bwd"},
+            "nccl_a2a_grouped_mm_baseline": None if nccl_gm_ms is None else {
+                "ms_per_step": nccl_gm_ms, "tokens_per_s": n * Tr / (nccl_gm_ms / 1000.0),
+                "speedup_of_fused": nccl_gm_ms / ms,
+                "what": "NCCL all_to_all_single dispatch/combine + one torch._grouped_mm (CUTLASS) per expert "
+                        "GEMM, bf16 SwiGLU / gate backward in torch ops"},
             "clocks": clk,
             "gpu_launches": int(launches),
             "gpu_launches_per_step": int(per_step_launches),
