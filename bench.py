@@ -772,6 +772,20 @@ def run_ours(args, cfg):
             "memory_bound_ops": membw,
             "exposed_comm": exposed,
             "graph_trace": None if gtrace is None else gtrace["summary"],
+            # expert-GEMM throughput inside the graph-replayed steps: this rank's real
+            # rows over each GEMM's busy time (max over ranks), vs the sustained peak
+            "gemm_tflops_in_step": None if gtrace is None else {
+                ph: {"busy_ms": gtrace["summary"]["phases_busy_ms"].get(ph),
+                     "tflops": fl / (gtrace["summary"]["phases_busy_ms"][ph] / 1000.0) / 1e12,
+                     "frac_sustained": fl / (gtrace["summary"]["phases_busy_ms"][ph] / 1000.0) / 1e12
+                                       / load_peaks()["bf16_sus"]}
+                for ph, fl in (("fc1", 2.0 * routing_info["local_rows"] * h * 2 * f),
+                               ("fc2", 2.0 * routing_info["local_rows"] * f * h),
+                               ("fc2_dgrad", 2.0 * routing_info["local_rows"] * h * f),
+                               ("fc1_dgrad", 2.0 * routing_info["local_rows"] * 2 * f * h),
+                               ("fc2_wgrad", 2.0 * routing_info["local_rows"] * h * f),
+                               ("fc1_wgrad", 2.0 * routing_info["local_rows"] * 2 * f * h))
+                if gtrace["summary"]["phases_busy_ms"].get(ph)},
             "nvlink": nvlink,
             "gemm_vs_cublas": gemm_cmp,
             "nvlink_dispatch_pull": nvlink_pull if membw is not None else None,
