@@ -27,6 +27,10 @@ CONFIGS = {
     "cfg3_deepseek": dict(h=7168, f=2048, E=256, k=8, route="learned", comm="bf16", gate="before_fc2_in", tol=1e-2),
     # configs[4]: Mixtral shape + FP8 communication + the reference's Zipf(1.2) routing
     "cfg5_fp8_zipf": dict(h=4096, f=14336, E=8, k=2, route="zipf", comm="fp8", gate="after_fc2_out", tol=5e-2),
+    # configs[4] with the reference test's capacity factor 1.0 (test_routing.cpp:82-97):
+    # group-capacity drops at EP > 1 (every rank one group, routing.cpp:113-131)
+    "cfg5_fp8_zipf_cf1": dict(h=4096, f=14336, E=8, k=2, route="zipf", comm="fp8", gate="after_fc2_out", tol=5e-2,
+                              cf=1.0),
 }
 ZIPF_FIXTURE = "routing_cfg5_zipf_nodrop_n8.npz"
 

@@ -38,7 +38,7 @@ def main():
     h, f, E, k = c["h"], c["f"], c["E"], c["k"]
     T, el = Tr * n, E // n
     w1, w2, wr, x, dy = make_inputs(c, T)
-    L = MoELayer(Tr, h, f, E, k, ep_size=n, rank=rank,
+    L = MoELayer(Tr, h, f, E, k, ep_size=n, rank=rank, capacity_factor=c.get("cf", 0.0),
                  route_mode="injected" if c["route"] == "zipf" else "learned",
                  gate_order=c["gate"], comm_format=c["comm"], ep_pattern=os.environ.get("MP_EP", "a2a"))
     L.set_weights(w1[rank * el:(rank + 1) * el].contiguous(), w2[rank * el:(rank + 1) * el].contiguous(), wr)
@@ -55,6 +55,11 @@ def main():
     L.status()
     r = L.routing()
     ex, gt, dr = (r[q].cpu().numpy() for q in ("experts", "gates", "dropped"))
+    if c.get("cf", 0.0) > 0:
+        # the layer's drops (replicated on every rank) = the pinned oracle's, routing.cpp:113-131
+        assert (P.orc_capacity_drop(ex, E, n, c["cf"]) == dr).all(), "capacity drops differ from the oracle"
+    else:
+        assert dr.sum() == 0
     toks, cols = sample(T, f, n_col=4)
 
     def gather(t):
@@ -92,7 +97,8 @@ def main():
         errs.update(dense_errors(P, c, ex, gt, dr, DG, toks, cols, x, dy, w1, w2, wr, Y[toks], DX[toks],
                                  G1, G2, dwr.cpu().numpy()))
         rows = [int((np.asarray(r2["row_map_in"]).size)) for r2 in maps]
-        print("MP_FULL_RESULT", name, n, {kk: f"{v:.2e}" for kk, v in errs.items()}, "rows_per_rank", rows, flush=True)
+        print("MP_FULL_RESULT", name, n, {kk: f"{v:.2e}" for kk, v in errs.items()}, "rows_per_rank", rows,
+              "dropped_tokens", int(dr.sum()), flush=True)
         bad = {kk: v for kk, v in errs.items() if kk != "logits" and not v < c["tol"]}
         assert not bad, bad
     dist.barrier()

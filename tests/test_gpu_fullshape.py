@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 T = 4096
 
 
-@pytest.mark.parametrize("name", list(CONFIGS))
+@pytest.mark.parametrize("name", [c for c in CONFIGS if "cf" not in CONFIGS[c]])
 def test_full_shape_sampled_parity(name):
     import pyoracle as P
     from conftest import GOLDEN

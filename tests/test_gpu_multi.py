@@ -68,7 +68,7 @@ def _run_full(n, cfg):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
-@pytest.mark.parametrize("cfg", ["cfg2_mixtral", "cfg3_deepseek", "cfg5_fp8_zipf"])
+@pytest.mark.parametrize("cfg", ["cfg2_mixtral", "cfg3_deepseek", "cfg5_fp8_zipf", "cfg5_fp8_zipf_cf1"])
 def test_ep4_full_shape_parity(cfg):
     """BASELINE configs[1], [2], [4] at EP = 4, T_r = 4096 per rank: sampled
     fwd+bwd parity against the oracle, every rank's scatter map bit-exact."""
