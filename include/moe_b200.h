@@ -360,8 +360,13 @@ moe_status moe_layer_ipc_import(moe_layer* L, const void* h_blobs);
 /* fp32 MoE layer forward on one GPU (BASELINE configs[0]): router (fp32;
  * skipped when d_experts_in/d_gates_in are given) -> capacity drop (cf <= 0:
  * none) -> permutation -> dispatch -> fc1 -> SwiGLU (-> gate) -> fc2 ->
- * gather -> combine, all in fp32 (FFMA expert GEMMs). Weights in the
- * reference layout w1 [E][2f][h] ([a|b] rows), w2 [E][h][f], wr [E][h]. */
+ * gather -> combine with fp32 accuracy (relative error ~5e-6): the expert
+ * GEMMs run on the tensor cores as bf16x6 (each operand split exactly into
+ * three bf16 pieces; MOE_F32_FFMA=1 selects FFMA grouped GEMMs). Stateless:
+ * work buffers come from the device's stream-ordered memory pool, whose
+ * release threshold the first call raises so they stay cached across calls.
+ * Weights in the reference layout w1 [E][2f][h] ([a|b] rows), w2 [E][h][f],
+ * wr [E][h]. */
 moe_status moe_ffn_forward_f32(const float* d_x, const float* d_w1, const float* d_w2,
                                const float* d_wr, int64_t T, int64_t h, int64_t f, int64_t E,
                                int64_t k, double capacity_factor, int32_t gate_order,
