@@ -74,7 +74,7 @@ moe_status attn_barrier(moe_attn* A, int slot, cudaStream_t s) {
     if (A->n == 1) return MOE_OK;
     flag_barrier_kernel<<<1, 64, 0, s>>>(reinterpret_cast<uint32_t* const*>(A->tab + 2 * A->n), slot,
                                         (int)A->n, (int)A->rank, A->epoch_dev, 1,
-                                        20ull * 1000 * 1000 * 1000, A->err);
+                                        flag_timeout_ns(), A->err);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;

@@ -180,7 +180,7 @@ moe_status fill(moe_dp* D) {
 moe_status dp_barrier(moe_dp* D, int slot, cudaStream_t s) {
     if (D->n == 1) return MOE_OK;
     flag_barrier_kernel<<<1, 64, 0, s>>>(reinterpret_cast<uint32_t* const*>(D->tab + D->n), slot, (int)D->n,
-                                        (int)D->rank, D->epoch_dev, 1, 20ull * 1000 * 1000 * 1000, D->err);
+                                        (int)D->rank, D->epoch_dev, 1, flag_timeout_ns(), D->err);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;

@@ -307,7 +307,7 @@ moe_status barrier(moe_layer* L, int slot, cudaStream_t s, int bump) {
     if (L->n == 1 || L->comm_local) return MOE_OK;
     if (!L->ipc_ready) return set_error(MOE_ERR_INVALID, "ep_size > 1 requires moe_layer_ipc_import");
     flag_barrier_kernel<<<1, 64, 0, s>>>(L->tab<uint32_t>(F_FLAGS), slot, (int)L->n, (int)L->rank,
-                                        L->epoch_dev, bump, 20ull * 1000 * 1000 * 1000, L->err,
+                                        L->epoch_dev, bump, flag_timeout_ns(), L->err,
                                         L->stamping ? L->stamps + PH_COUNT + 2 * slot : nullptr, (int)L->debug);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());

@@ -1,6 +1,7 @@
 // runtime.cu — status plumbing, launch accounting, TMA descriptor encoding
 // and the C-ABI entry points of the routing / quantisation operators.
 #include <atomic>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -59,6 +60,15 @@ moe_status make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType 
                          (int)r, (unsigned long long)inner, (unsigned long long)outer,
                          (unsigned long long)row_bytes, box_inner, box_outer);
     return MOE_OK;
+}
+
+unsigned long long flag_timeout_ns() {
+    static const unsigned long long ns = [] {
+        const char* e = getenv("MOE_FLAG_TIMEOUT_MS");
+        const long long ms = e ? atoll(e) : 0;
+        return (unsigned long long)(ms > 0 ? ms : 20000) * 1000ull * 1000ull;
+    }();
+    return ns;
 }
 
 moe_status flag_status(const int* d_err, cudaStream_t s, const char* what) {

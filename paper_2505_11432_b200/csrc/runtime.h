@@ -45,6 +45,10 @@ moe_status launch_balance_counts(const int32_t* experts, const uint8_t* dropped,
                                  int64_t E, int64_t k, int64_t n, int64_t* load,
                                  int64_t* assigned, int64_t* ndrop, cudaStream_t s);
 
+// Bound of a cross-GPU flag barrier wait before it gives up and sets the
+// error flag (MOE_FLAG_TIMEOUT_MS, default 20000 ms; read once).
+unsigned long long flag_timeout_ns();
+
 // Device error flag of a handle -> status: synchronises `s`, then returns
 // MOE_ERR_TIMEOUT when a bounded cross-GPU wait gave up (1 = flag barrier,
 // 2 = fused-dispatch row wait, 3 = DP in-place cast wait).

@@ -69,7 +69,7 @@ moe_status u_barrier(moe_ulysses* U, int slot, cudaStream_t s) {
     if (U->n == 1) return MOE_OK;
     flag_barrier_kernel<<<1, 64, 0, s>>>(reinterpret_cast<uint32_t* const*>(U->tab + 2 * U->n), slot,
                                         (int)U->n, (int)U->rank, U->epoch_dev, 1,
-                                        20ull * 1000 * 1000 * 1000, U->err);
+                                        flag_timeout_ns(), U->err);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
     return MOE_OK;

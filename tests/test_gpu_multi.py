@@ -111,3 +111,15 @@ def test_ep2_protocol_assertions(ep):
     every slot, every dispatch block landed exactly once, dedup rows once,
     all-gather chunks complete — over several steps, with drops and dedup."""
     _run(2, {"MP_CF": "1.25", "MP_E": "8", "MP_K": "4", "MP_TR": "256", "MP_EP": ep, "MOE_DEBUG_CHECKS": "1"})
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_ep2_timeout_status():
+    """A peer that never arrives: the bounded flag waits give up and the status
+    path returns MOE_ERR_TIMEOUT (no hang, no silent success)."""
+    env = dict(os.environ, MOE_FLAG_TIMEOUT_MS="1500")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29651", os.path.join(ROOT, "tests", "mp_timeout_check.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "TIMEOUT_RESULT ok" in p.stdout
