@@ -9,12 +9,18 @@
 //            by block, and the TMA producer waits per block (identity
 //            permutation of the MoE dispatch path, k = 1).
 //   GEMM-RS  y_r[s/n, h] = sum over ranks of (o[s, h/n] . Wout_r[h, h/n]^T)
-//            the epilogue stores every output row into the owning rank's
-//            staging slot (row, source rank); after a device flag barrier the
-//            owner sums the n partials in fixed rank order in fp32
-//            (a2a_fp32 reduction semantics, numerics.cpp:172-192).
+//            tiles are taken shard by shard, peers' shards first (rank+1, ...)
+//            and this rank's own shard last. A peer shard's tile is stored to
+//            the owner's staging slot (row, source rank) and counted on the
+//            owner's per-tile counter; an own tile waits for its n-1 counts and
+//            its epilogue sums the n partials in fixed rank order in fp32
+//            (a2a_fp32 reduction semantics, numerics.cpp:172-192) straight into
+//            y: no trailing barrier, no separate reduce kernel
+//            (MOE_ATTN_RS_UNFUSED=1 at create: staging for every tile, flag
+//            barrier, then the reduce kernel).
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "gemm.h"
@@ -27,13 +33,15 @@ struct moe_attn {
     int64_t s = 0, h = 0, nq = 0, dh = 0, n = 1, rank = 0, sr = 0;  // sr = s / n
     int cg = 2;
     uint8_t* arena = nullptr;
-    size_t off_x = 0, off_stage = 0, off_flags = 0, arena_bytes = 0;
+    size_t off_x = 0, off_stage = 0, off_flags = 0, off_rscnt = 0, arena_bytes = 0;
     std::vector<uint8_t*> peer;
-    void** tab = nullptr;  // [3][n]: x shards, staging, flags
+    void** tab = nullptr;  // [4][n]: x shards, staging, flags, GEMM-RS tile counters
     uint16_t *x_all = nullptr, *wqkv = nullptr, *wout = nullptr;
     int32_t *ident = nullptr, *rows_s = nullptr, *rows_pad = nullptr, *row_dst = nullptr;
     uint32_t* ready = nullptr;
     uint32_t* epoch_dev = nullptr;
+    uint32_t* rs_epoch = nullptr;   // GEMM-RS calls so far (the start barrier bumps it)
+    bool rs_fused = true;
     int* err = nullptr;
     int* counters = nullptr;  // dynamic tile schedule, one per plan
     bool ipc_ready = false, weights = false;
@@ -60,20 +68,21 @@ __global__ void attn_rows_kernel(int32_t* ident, int32_t* row_dst, int s, int sr
 
 moe_status fill(moe_attn* A) {
     const int n = (int)A->n;
-    std::vector<void*> t(3 * n);
+    std::vector<void*> t(4 * n);
     for (int p = 0; p < n; ++p) {
         t[p] = A->peer[p] + A->off_x;
         t[n + p] = A->peer[p] + A->off_stage;
         t[2 * n + p] = A->peer[p] + A->off_flags;
+        t[3 * n + p] = A->peer[p] + A->off_rscnt;
     }
     MOE_CUDA_TRY(cudaMemcpy(A->tab, t.data(), sizeof(void*) * t.size(), cudaMemcpyHostToDevice));
     return MOE_OK;
 }
 
-moe_status attn_barrier(moe_attn* A, int slot, cudaStream_t s) {
+moe_status attn_barrier(moe_attn* A, int slot, cudaStream_t s, uint32_t* epoch = nullptr) {
     if (A->n == 1) return MOE_OK;
     flag_barrier_kernel<<<1, 64, 0, s>>>(reinterpret_cast<uint32_t* const*>(A->tab + 2 * A->n), slot,
-                                        (int)A->n, (int)A->rank, A->epoch_dev, 1,
+                                        (int)A->n, (int)A->rank, epoch ? epoch : A->epoch_dev, 1,
                                         flag_timeout_ns(), A->err);
     count_launch();
     MOE_CUDA_TRY(cudaGetLastError());
@@ -106,14 +115,16 @@ moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_ran
     A->off_x = take(A->sr * A->h * 2);
     A->off_stage = take(A->sr * A->n * A->h * 2);
     A->off_flags = take(16 * 64 * 4);
+    A->off_rscnt = take((A->sr / (128 * A->cg)) * (A->h / 256) * 4);
     A->arena_bytes = off;
+    A->rs_fused = getenv("MOE_ATTN_RS_UNFUSED") == nullptr;
     moe_status st;
 #define TRY(expr) do { st = (expr); if (st != MOE_OK) { moe_attn_destroy(A); return st; } } while (0)
     TRY(dalloc(&A->arena, A->arena_bytes));
     cudaMemset(A->arena, 0, A->arena_bytes);
     A->peer.assign(A->n, nullptr);
     A->peer[A->rank] = A->arena;
-    TRY(dalloc(&A->tab, 3 * A->n));
+    TRY(dalloc(&A->tab, 4 * A->n));
     TRY(dalloc(&A->x_all, A->s * A->h));
     TRY(dalloc(&A->wqkv, A->nq * A->h));
     TRY(dalloc(&A->wout, A->h * A->dh));
@@ -123,6 +134,8 @@ moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_ran
     TRY(dalloc(&A->rows_pad, 1));
     TRY(dalloc(&A->ready, A->s / 128 + 2));  // + the dispatch row-claim counter
     TRY(dalloc(&A->epoch_dev, 1));
+    TRY(dalloc(&A->rs_epoch, 1));
+    cudaMemset(A->rs_epoch, 0, 4);
     TRY(dalloc(&A->err, 1));
     TRY(dalloc(&A->counters, 2));
     cudaMemset(A->epoch_dev, 0, 4);
@@ -160,7 +173,7 @@ moe_status moe_attn_create(int64_t seq, int64_t hidden, int64_t qkv_cols_per_ran
     TRY(tmap_kmajor(&A->p_qkv.tb, A->wqkv, A->nq, A->h, A->p_qkv.bn / A->cg));
     A->p_qkv.counter = A->counters;
     A->p_out.cg = A->cg;
-    A->p_out.epi = EPI_SCATTER;
+    A->p_out.epi = A->rs_fused ? EPI_SCATTER_RS : EPI_SCATTER;
     A->p_out.counter = A->counters + 1;
     TRY(tmap_kmajor(&A->p_out.tb, A->wout, A->h, A->dh, 256 / A->cg));
 #undef TRY
@@ -178,7 +191,7 @@ void moe_attn_destroy(moe_attn* A) {
     for (int p = 0; p < (int)A->peer.size(); ++p)
         if (p != A->rank && A->peer[p]) cudaIpcCloseMemHandle(A->peer[p]);
     void* bufs[] = {A->arena, A->tab, A->x_all, A->wqkv, A->wout, A->ident, A->row_dst, A->rows_s,
-                    A->rows_pad, A->ready, A->epoch_dev, A->err, A->counters};
+                    A->rows_pad, A->ready, A->epoch_dev, A->rs_epoch, A->err, A->counters};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete A;
@@ -237,7 +250,6 @@ moe_status moe_attn_gemm_rs(moe_attn* A, const uint16_t* d_o, uint16_t* d_y_shar
     cudaStream_t s = (cudaStream_t)stream;
     GemmPlan p = A->p_out;
     MOE_TRY(tmap_kmajor(&p.ta, d_o, A->s, A->dh, 128));
-    MOE_TRY(attn_barrier(A, 1, s));  // owners finished reading the previous staging
     GemmArgs a{};
     a.G = 1;
     a.group_rows = A->rows_s;
@@ -247,11 +259,32 @@ moe_status moe_attn_gemm_rs(moe_attn* A, const uint16_t* d_o, uint16_t* d_y_shar
     a.ldo = A->h;
     a.row_dst = A->row_dst;
     a.rank_base = reinterpret_cast<void* const*>(A->tab + A->n);
-    // own rows first, then owner rank+1, ...: at any time the ranks push to different owners
+    a.err = A->err;
+    if (A->rs_fused) {
+        // owners finished reading the previous call's staging; bumps the call count
+        MOE_TRY(attn_barrier(A, 1, s, A->rs_epoch));   // (n = 1: nothing to wait for)
+        const int tm = 128 * A->cg;
+        const int n_tiles = (int)(A->h / 256);
+        static const int delay_env = getenv("MOE_ATTN_RS_DELAY") ? atoi(getenv("MOE_ATTN_RS_DELAY")) : 6;
+        a.rs_order = 1;
+        a.rs_delay = std::max(0, std::min(delay_env, n_tiles - 1));
+        a.self_rank = (int)A->rank;
+        a.rs_cnt = reinterpret_cast<uint32_t* const*>(A->tab + 3 * A->n);
+        a.rs_epoch = A->rs_epoch;
+        a.rs_out = d_y_shard;
+        a.rs_rows = (int)A->sr;
+        a.rs_n = (int)A->n;
+        a.rs_tile_m = tm;
+        a.rs_tile_warps = 8 * A->cg;
+        return gemm_launch(p, a, s);
+    }
+    MOE_TRY(attn_barrier(A, 1, s));  // owners finished reading the previous staging
+    // m-tiles of every column start at the own shard; each column interleaves
+    // all owners, so the link carries the pushes for the whole GEMM
     a.m_rot = (int)(A->rank * A->sr / (128 * A->cg));
     MOE_TRY(gemm_launch(p, a, s));
     MOE_TRY(attn_barrier(A, 2, s));
-    launch_combine<false>(s, 
+    launch_combine<false>(s,
         A->arena + A->off_stage, nullptr, nullptr, (int)A->sr, (int)A->n, (int)A->h, d_y_shard,
         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     count_launch();

@@ -33,7 +33,7 @@ static moe_status launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, cons
                               int grid, cudaStream_t s) {
     using Cfg = GemmCfg<BN, CG>;
     auto kern = grouped_gemm_kernel<BN, CG, A_MN, B_MN, KG, EPI, DISP>;
-    constexpr int kThreads = Cfg::THREADS + (DISP ? 32 * Cfg::COMM_WARPS : 0);
+    constexpr int kThreads = Cfg::THREADS + (DISP ? 32 * Cfg::COMM_WARPS : 0) + (EPI == EPI_SCATTER_RS ? 32 : 0);
     static uint64_t attr_set = 0;  // per instantiation, one bit per device
     int dev = 0;
     MOE_CUDA_TRY(cudaGetDevice(&dev));
@@ -102,6 +102,7 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     MOE_GEMM_CASE(256, 2, false, true, false, EPI_SWIGLU_BWD)    // fc2 dgrad
     MOE_GEMM_CASE(256, 2, false, true, false, EPI_SCATTER)       // fc1 dgrad
     MOE_GEMM_CASE(256, 2, false, false, false, EPI_SCATTER_FP8)  // fc2 + FP8 combine payload
+    MOE_GEMM_CASE(256, 2, false, false, false, EPI_SCATTER_RS)   // TP GEMM-RS, fused reduce
     MOE_GEMM_CASE(256, 2, false, true, false, EPI_SCATTER_FP8)   // fc1 dgrad + FP8 payload
     MOE_GEMM_CASE(256, 2, true, true, true, EPI_STORE_BF16)      // wgrads
     MOE_GEMM_CASE(256, 2, true, true, true, EPI_STORE_F32)
@@ -113,6 +114,7 @@ moe_status gemm_launch(const GemmPlan& p, const GemmArgs& args, cudaStream_t s) 
     MOE_GEMM_CASE(256, 1, false, false, false, EPI_SWIGLU)
     MOE_GEMM_CASE(256, 1, false, false, false, EPI_SCATTER)
     MOE_GEMM_CASE(256, 1, false, false, false, EPI_SCATTER_FP8)
+    MOE_GEMM_CASE(256, 1, false, false, false, EPI_SCATTER_RS)
     MOE_GEMM_CASE(256, 1, false, true, false, EPI_SCATTER_FP8)
     MOE_GEMM_CASE(256, 1, false, true, false, EPI_SWIGLU_BWD)
     MOE_GEMM_CASE(256, 1, false, true, false, EPI_SCATTER)

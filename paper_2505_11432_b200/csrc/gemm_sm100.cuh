@@ -39,6 +39,8 @@ enum EpiKind : int {
     EPI_SCATTER = 3,      // fc2 / fc1-dgrad: rows -> (rank, slot row) staging
     EPI_SWIGLU_BWD = 4,   // fc2-dgrad: SwiGLU+gate backward, remat fc2_in, dgate partials
     EPI_SCATTER_FP8 = 5,  // EPI_SCATTER with grouped-128 E4M3 payload + fp32 scales (FP8 comm)
+    EPI_SCATTER_RS = 6,   // TP GEMM-RS: peer-owned tiles -> owner staging + per-tile count;
+                          // own tiles (taken last) reduce the n partials into y in rank order
 };
 
 struct GemmArgs {
@@ -113,6 +115,22 @@ struct GemmArgs {
     // takes tiles in order with an atomic and hands them to every role through a
     // shared-memory queue (nullptr = static stride schedule)
     int* tile_counter;
+    // TP GEMM-RS with the reduction fused into the GEMM (EPI_SCATTER_RS; reference
+    // out_proj -> rs_attn_out, graph.cpp:208-214): rows are split into owner shards
+    // of rs_rows. A tile of a peer's shard is stored to that owner's staging
+    // rank_base[owner] at row (local row * rs_n + self_rank), then every epilogue
+    // warp adds 1 to the owner's rs_cnt[owner][tile] (release, system scope). A
+    // tile of this rank's own shard waits until its counter reaches
+    // *rs_epoch * (epilogue warps per tile) * (rs_n - 1), then writes
+    // y = sum over ranks r (in rank order, fp32) of bf16(partial_r) to rs_out —
+    // the same values and order as the unfused staging + combine.
+    uint32_t* const* rs_cnt;
+    const uint32_t* rs_epoch;
+    uint16_t* rs_out;
+    int rs_rows, rs_n;
+    int rs_tile_m, rs_tile_warps;   // rows per tile, epilogue warps per tile (both CTAs)
+    int rs_order, rs_delay;         // 1: fused GEMM-RS tile order (decode_tile), own tiles of a
+                                    // column rs_delay blocks after the peers'
 };
 
 template <int BN, int CG>
@@ -157,6 +175,31 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
     if (!K_GROUPED) {
         const int rows = row_off[lo + 1] - row_off[lo];
         const int mt = (rows + TILE_M - 1) / TILE_M;
+        if (a.rs_order) {
+            // fused GEMM-RS order: block c = the peer shards' tiles of column c
+            // (shards self+1, self+2, ...) followed by this rank's own tiles of
+            // column c - D; peers reach a column D blocks before its owner
+            // reduces it, and every block keeps the link busy
+            const int tps = a.rs_rows / TILE_M, P = (a.rs_n - 1) * tps, D = a.rs_delay;
+            int c, r;
+            bool own;
+            if (li < D * P) {
+                c = li / P; r = li - c * P; own = false;
+            } else if (li < D * P + (n_tiles - D) * (P + tps)) {
+                const int l2 = li - D * P;
+                c = D + l2 / (P + tps); r = l2 % (P + tps);
+                own = r >= P;
+                if (own) { r -= P; c -= D; }
+            } else {
+                const int l3 = li - D * P - (n_tiles - D) * (P + tps);
+                c = n_tiles - D + l3 / tps; r = l3 % tps; own = true;
+            }
+            ti.n = c;
+            ti.m = own ? a.self_rank * tps + r : ((a.self_rank + 1) * tps + r) % mt;
+            ti.kblocks = (a.K + 63) / 64;
+            ti.row0 = row_off[lo] + ti.m * TILE_M;
+            return ti;
+        }
         const int mc = (a.m_chunk > 0 && a.m_chunk < mt) ? a.m_chunk : mt;
         const int full = mc * n_tiles;
         const int c = li / full;
@@ -366,6 +409,16 @@ __device__ __forceinline__ void load_rows32_issue_s(uint4 (&v)[4], const void* r
     }
 }
 
+// Same, through L2 only (.cg): rows a peer wrote over NVLink in this launch
+__device__ __forceinline__ void load_rows32_issue_cg_s(uint4 (&v)[4], const void* row_ptr, int64_t stride, int lane) {
+    const char* row0 = reinterpret_cast<const char*>(row_ptr) - (int64_t)lane * stride;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int R = (lane >> 2) + 8 * i, c = lane & 3;
+        v[i] = __ldcg(reinterpret_cast<const uint4*>(row0 + (int64_t)R * stride) + c);
+    }
+}
+
 // Issue the coalesced global loads of a 32 x 32 bf16 chunk (4 x 16 B per lane).
 __device__ __forceinline__ void load_rows32_issue(uint4 (&v)[4], const void* row_ptr, int lane) {
     const unsigned long long my = reinterpret_cast<unsigned long long>(row_ptr);
@@ -500,6 +553,86 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             }
             *reinterpret_cast<uint4*>(codes + c0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             *reinterpret_cast<uint4*>(codes + c0 + 16) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+    } else if constexpr (EPI == EPI_SCATTER_RS) {
+        const int nr = args.rs_n, self = args.self_rank;
+        const int owner = ti.row0 / args.rs_rows;
+        const int64_t lrow = orow - (int64_t)owner * args.rs_rows;
+        const int64_t sstride = (int64_t)nr * args.ldo * 2;   // bytes between a warp's staging rows
+        if (owner != self) {
+            uint16_t* obf = reinterpret_cast<uint16_t*>(args.rank_base[owner]) + (lrow * nr + self) * args.ldo + n0;
+#pragma unroll 1
+            for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tbase + (c0 - tshift), r);
+                tmem_ld_wait();
+                uint32_t pk[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+                store_rows32_s(wst, pk, obf + c0, sstride, lane);
+            }
+        } else {
+            if (lane == 0 && nr > 1) {
+                const int idx = (ti.m - owner * (args.rs_rows / args.rs_tile_m)) * n_tiles + ti.n;
+                const uint32_t target = *args.rs_epoch * (uint32_t)args.rs_tile_warps * (uint32_t)(nr - 1);
+                const uint32_t* cnt = args.rs_cnt[self] + idx;
+                const uint64_t t0 = globaltimer();
+                while ((int32_t)(ld_acquire_sys(cnt) - target) < 0) {
+                    if (globaltimer() - t0 > 4000000000ull) {
+                        atomicExch(args.err, 4);
+                        break;
+                    }
+                }
+            }
+            __syncwarp();
+            const uint16_t* stage = reinterpret_cast<const uint16_t*>(args.rank_base[self]) + lrow * nr * args.ldo + n0;
+            uint16_t* y = args.rs_out + lrow * args.ldo + n0;
+#pragma unroll 1
+            for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
+                uint32_t own[16];
+                {
+                    uint32_t r[32];
+                    tmem_ld32(tbase + (c0 - tshift), r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) own[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+                }
+                float acc[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) acc[q] = 0.0f;
+                // fixed rank order, fp32 sum of bf16 partials (combine_reduce_kernel)
+#pragma unroll 1
+                for (int s0 = 0; s0 < nr; s0 += 4) {
+                    uint4 v[4][4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int src = s0 + j;
+                        if (src < nr && src != self) load_rows32_issue_cg_s(v[j], stage + src * args.ldo + c0, sstride, lane);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int src = s0 + j;
+                        if (src >= nr) break;
+                        uint32_t w[16];
+                        if (src == self) {
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) w[q] = own[q];
+                        } else {
+                            load_rows32_finish(wst, v[j], w, lane);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            const float2 f = unpack_bf16x2(w[q]);
+                            acc[2 * q] += f.x;
+                            acc[2 * q + 1] += f.y;
+                        }
+                    }
+                }
+                uint32_t pk[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(acc[2 * q], acc[2 * q + 1]);
+                store_rows32_s(wst, pk, y + c0, args.ldo * 2, lane);
+            }
         }
     } else if constexpr (EPI == EPI_SWIGLU) {
         // W1 rows are packed per 128-row block as [a 64 | b 64] (pack_w1_kernel),
@@ -761,7 +894,8 @@ __device__ __forceinline__ void dispatch_warp(const GemmArgs& a, int K, int lane
 }
 
 template <int BN, int CG, bool A_MN, bool B_MN, bool K_GROUPED, int EPI, bool DISPATCH = false>
-__global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * GemmCfg<BN, CG>::COMM_WARPS : 0), 1)
+__global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * GemmCfg<BN, CG>::COMM_WARPS : 0) +
+                                  (EPI == EPI_SCATTER_RS ? 32 : 0), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
     using Cfg = GemmCfg<BN, CG>;
@@ -782,6 +916,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     constexpr int QD = 8;                           // tile queue depth
     __shared__ int s_tq[QD];
     __shared__ __align__(8) uint64_t s_tq_full[QD], s_tq_empty[QD];
+    // EPI_SCATTER_RS: epilogue warps -> signal warp ring (one entry per tile)
+    constexpr int QS = 8;
+    __shared__ __align__(8) uint64_t s_sig_full[QS], s_sig_free[QS];
+    __shared__ int s_sig_info[QS];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -851,6 +989,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             mbar_init(&s_tq_full[q], 1);
             mbar_init(&s_tq_empty[q], (1 + Cfg::EPI_WARPS) * CG);
         }
+        if (EPI == EPI_SCATTER_RS)
+            for (int q = 0; q < QS; ++q) {
+                mbar_init(&s_sig_full[q], Cfg::EPI_WARPS);
+                mbar_init(&s_sig_free[q], 1);
+            }
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -1090,6 +1233,31 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
                 mma_role(std::true_type{});
             }
         }
+    } else if (EPI == EPI_SCATTER_RS && warp == 2 + Cfg::EPI_WARPS) {
+        // ===================== GEMM-RS signal warp =====================
+        // Announces this CTA's part of each peer-owned tile once its 8 epilogue
+        // warps stored it: the CTA-scope mbarrier orders their NVLink stores
+        // before this lane's system-scope release, so the epilogue warps never
+        // wait for the link to drain.
+        // Entries that completed while a fence drained are announced together
+        // behind one fence (one link drain per batch, not per tile).
+        if (lane == 0) {
+            bool done = false;
+            for (int sq = 0; !done;) {
+                mbar_wait(&s_sig_full[sq % QS], (uint32_t)(sq / QS) & 1u);
+                int end = sq + 1;
+                while (end - sq < QS && mbar_try_wait(&s_sig_full[end % QS], (uint32_t)(end / QS) & 1u)) ++end;
+                fence_acq_rel_sys();
+                for (int q = sq; q < end; ++q) {
+                    const int info = *reinterpret_cast<volatile int*>(&s_sig_info[q % QS]);
+                    if (info >= 0)
+                        red_relaxed_sys_add(args.rs_cnt[info >> 24] + (info & 0xffffff), (uint32_t)Cfg::EPI_WARPS);
+                    if (info == -2) done = true;
+                    mbar_arrive(&s_sig_free[q % QS]);
+                }
+                sq = end;
+            }
+        }
     } else if (DISPATCH && warp >= 2 + Cfg::EPI_WARPS) {
         // ===================== dispatch (comm warps) =====================
         dispatch_warp<TILE_M>(args, args.K, lane);
@@ -1102,9 +1270,27 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
         const uint32_t tempty_leader = CG == 2 ? map_to_cta(&tempty_bar[0], 0) : 0;
         int acc = 0;
         uint32_t acc_phase = 0;
+        int sig_sq = 0;
+        // EPI_SCATTER_RS: publish one ring entry per tile (warp 0 of the epilogue
+        // writes it once the signal warp freed the slot; all 8 warps arrive after
+        // their stores, which orders those stores before the signal warp's release)
+        auto rs_sig = [&](int sq, int info) {
+            const int slot = sq % QS;
+            __syncwarp();
+            if (lane == 0) {
+                if (ew == 0) {
+                    mbar_wait(&s_sig_free[slot], ((uint32_t)(sq / QS) & 1u) ^ 1u);
+                    s_sig_info[slot] = info;
+                }
+                mbar_arrive(&s_sig_full[slot]);
+            }
+        };
         for (int it = 0;; ++it) {
             const int t = next_tile(it);
-            if (t < 0) break;
+            if (t < 0) {
+                if (EPI == EPI_SCATTER_RS) rs_sig(sig_sq, -2);
+                break;
+            }
             const TileInfo ti = decode_tile<TILE_M, K_GROUPED>(t, prefix, s_rowoff, s_kb, args, G, n_tiles);
             const int n0 = ti.n * BN;
             int64_t orow;
@@ -1163,6 +1349,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
             if (lane == 0) {
                 if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
                 else mbar_arrive(&tempty_bar[acc]);
+            }
+            if constexpr (EPI == EPI_SCATTER_RS) {
+                // hand the tile to the signal warp (peer-owned: owner and tile index)
+                const int owner = ti.row0 / args.rs_rows;
+                const int info = owner != args.self_rank
+                                     ? (owner << 24) | ((ti.m - owner * (args.rs_rows / TILE_M)) * n_tiles + ti.n)
+                                     : -1;
+                rs_sig(sig_sq++, info);
             }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }

@@ -82,10 +82,10 @@ moe_status flag_status(const int* d_err, cudaStream_t s, const char* what) {
                          : v == 10 ? "deduplicated row not landed exactly once" : v == 11 ? "all-gather chunk incomplete"
                          : "barrier epoch mismatch (16 + slot)");
     static const char* kinds[] = {"", "cross-GPU flag barrier", "fused-dispatch row arrival",
-                                  "DP in-place cast chunk"};
+                                  "DP in-place cast chunk", "GEMM-RS tile arrival"};
     return set_error(MOE_ERR_TIMEOUT, "%s: a %s wait exceeded its bound (a peer rank stalled or "
                      "failed); results of the affected calls are invalid", what,
-                     (v >= 1 && v <= 3) ? kinds[v] : "device");
+                     (v >= 1 && v <= 4) ? kinds[v] : "device");
 }
 
 }  // namespace moe

@@ -34,6 +34,21 @@ def main():
         y = A.gemm_rs(o[:, rank * dh:(rank + 1) * dh].contiguous().cuda())
     torch.cuda.synchronize()
     assert A.error_flag() == 0
+    # the fused GEMM-RS (reduction in the own-shard tiles' epilogue) against the
+    # unfused staging + barrier + reduce kernel: same partials, same rank order
+    os.environ["MOE_ATTN_RS_UNFUSED"] = "1"
+    B = AttnProjections(s, h, nq, n, rank)
+    del os.environ["MOE_ATTN_RS_UNFUSED"]
+    B.set_weights(wqkv[rank].cuda(), wout[:, rank * dh:(rank + 1) * dh].contiguous().cuda())
+    if n > 1:
+        B.connect()
+    y_unfused = B.gemm_rs(o[:, rank * dh:(rank + 1) * dh].contiguous().cuda())
+    torch.cuda.synchronize()
+    assert B.error_flag() == 0
+    same = torch.tensor([float(torch.equal(y, y_unfused))], device="cuda")
+    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    assert same.item() == 1.0, "fused GEMM-RS differs from staging + reduce"
+    A.status()
     ref_qkv = x.float() @ wqkv[rank].float().T
     ref_y = (o.float() @ wout.float().T)[rank * sr:(rank + 1) * sr]
     e1 = ((qkv.float().cpu() - ref_qkv).norm() / ref_qkv.norm()).item()
