@@ -321,7 +321,8 @@ def run_ours(args, cfg):
     injected = "routing_fixture" in cfg
     L = MoELayer(Tr, h, f, E, k, ep_size=n, rank=rank, capacity_factor=0.0,
                  gate_order=cfg.get("gate", "before_fc2_in"), comm_format=cfg.get("comm", "bf16"),
-                 route_mode="injected" if injected else "learned", ep_pattern=args.ep_pattern)
+                 route_mode="injected" if injected else "learned", ep_pattern=args.ep_pattern,
+                 remat=not args.no_remat)
     L.set_weights(w1, w2, wr)
     if injected:
         # routing input data: the reference's simulate_routing output (committed fixture)
@@ -659,6 +660,22 @@ def run_ours(args, cfg):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te.item())
+    # the same host copies alone (every rank at once, no compute): the floor the
+    # host link puts under the e2e step
+    sync_all()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(cs):
+        c0.record(cs)
+        for i in range(args.steps):
+            xb[i % 2].copy_(x_h, non_blocking=True)
+            dyb[i % 2].copy_(dy_h, non_blocking=True)
+            dx_h.copy_(dxb[i % 2], non_blocking=True)
+        c1.record(cs)
+    sync_all()
+    tc = torch.tensor([c0.elapsed_time(c1) / args.steps], device="cuda")
+    if world > 1:
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+    copy_only_ms = float(tc.item())
 
     rt = L.routing()
     cnt = rt["per_expert_counts"].cpu().tolist()[rank * el:(rank + 1) * el]
@@ -790,6 +807,7 @@ def run_ours(args, cfg):
                        "top_k": k, "tokens_per_rank": Tr, "global_tokens": Tr * n,
                        "parallelism": f"ep{n}", "comm_format": cfg.get("comm", "bf16"),
                        "gate_order": cfg.get("gate", "before_fc2_in"), "ep_pattern": args.ep_pattern,
+                       "remat": "off" if args.no_remat else "selective",
                        "l2": "inputs larger than L2 (expert weights >= 2.8 GB/layer)"},
             "roofline": roof,
             "phases_ms": {kk: round(v, 4) for kk, v in phases.items()},
@@ -829,7 +847,7 @@ def run_ours(args, cfg):
             "launch_mode": "eager" if args.no_graph else "cuda_graph",
             "e2e": {"value": n * Tr / (e2e_ms / 1000.0), "unit": "tokens/s",
                     "h2d_bytes_per_step": 2 * Tr * h * 2, "d2h_bytes_per_step": Tr * h * 2,
-                    "ms_per_step": e2e_ms,
+                    "ms_per_step": e2e_ms, "host_copies_only_ms_per_step": copy_only_ms,
                     "mode": ("MoELayer.forward/backward captured as one CUDA graph per buffer set; x, dy "
                              "uploaded and dx read back every step from pinned host memory on a copy stream"
                              if not args.no_graph else "eager MoELayer.forward/backward calls; same copies")},
@@ -1295,6 +1313,8 @@ def main():
     ap.add_argument("--ep-pattern", default="a2a", choices=["a2a", "ag_rs"],
                     help="EP dispatch/combine pattern (commcost.hpp:81): needed-row pulls + per-slot pushes, "
                          "or all-gather + local scatter and per-rank pre-reduced reduce-scatter")
+    ap.add_argument("--no-remat", action="store_true",
+                    help="RematPolicy::off (reference --no-remat): keep the forward's fc2_in for the fc2 wgrad")
     ap.add_argument("--trace", default=None, help="write the measured per-phase timeline (reference trace schema)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -189,6 +189,10 @@ typedef struct {
     int32_t ffn_norm;        /* 1: RMSNorm (reference node ffn_norm, graph.cpp:267) fused ahead of
                                 the router and the dispatch; its backward follows the dx combine */
     float norm_eps;
+    int32_t no_remat;        /* 0 (reference default, RematPolicy::selective, memmodel.cpp:25-31):
+                                fc2_in is recomputed from fc1_out in the fc2-dgrad epilogue;
+                                1 (`--no-remat`, RematPolicy::off): the forward's fc2_in is kept
+                                for the fc2 weight gradient and not rewritten */
 } moe_layer_config;
 
 moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out);

@@ -670,7 +670,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         const float g = args.row_gate ? args.row_gate[orow] : 1.0f;
         const uint16_t* f1 = args.aux + orow * args.ld_aux;
         uint16_t* d1 = reinterpret_cast<uint16_t*>(args.out) + orow * args.ldo;
-        uint16_t* rf = reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2;
+        uint16_t* rf = args.out2 ? reinterpret_cast<uint16_t*>(args.out2) + orow * args.ldo2 : nullptr;
         float dg = 0.0f;
         // va / vb: the first chunk's fc1_out rows, issued by the caller before it
         // waited for the accumulator; chunk c+1's loads fly during chunk c's stores
@@ -707,7 +707,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             }
             store_rows32(wst, da, d1 + ia, lane);
             store_rows32(wst, db, d1 + ia + 64, lane);
-            store_rows32(wst, hf, rf + j, lane);
+            if (rf) store_rows32(wst, hf, rf + j, lane);   // remat (RematPolicy::selective)
         }
         if (args.row_part) args.row_part[orow * (2 * n_tiles) + ti.n * 2 + half] = dg;
     }

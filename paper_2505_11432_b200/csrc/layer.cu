@@ -893,7 +893,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         a.b_group_stride = (int)h;
         a.out = L->dfc1;
         a.ldo = 2 * f;
-        a.out2 = L->fc2_in;
+        a.out2 = L->cfg.no_remat ? nullptr : L->fc2_in;   // nullptr: keep the forward's fc2_in
         a.ldo2 = f;
         a.aux = L->fc1_out;
         a.ld_aux = 2 * f;

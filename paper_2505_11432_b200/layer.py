@@ -20,7 +20,7 @@ class _Cfg(C.Structure):
                 ("num_experts", C.c_int64), ("top_k", C.c_int64), ("ep_size", C.c_int64),
                 ("rank", C.c_int64), ("capacity_factor", C.c_double), ("gate_order", C.c_int32),
                 ("comm_format", C.c_int32), ("ep_pattern", C.c_int32), ("route_mode", C.c_int32),
-                ("ffn_norm", C.c_int32), ("norm_eps", C.c_float)]
+                ("ffn_norm", C.c_int32), ("norm_eps", C.c_float), ("no_remat", C.c_int32)]
 
 
 class _RoutingView(C.Structure):
@@ -65,16 +65,20 @@ class MoELayer:
                  top_k: int, ep_size: int = 1, rank: int = 0, capacity_factor: float = 0.0,
                  gate_order: str = "before_fc2_in", comm_format: str = "bf16",
                  route_mode: str = "learned", ffn_norm: bool = False, norm_eps: float = 1e-6,
-                 ep_pattern: str = "a2a"):
+                 ep_pattern: str = "a2a", remat: bool = True):
         """ep_pattern (commcost.hpp:81): "a2a" = pull only the rows this rank's
         experts need + push every (token, slot) output row to its owner;
         "ag_rs" = all-gather every token row, local scatter, and one
         pre-reduced partial row per (token, serving rank) reduce-scattered to
-        the owner (bf16 communication, gate before fc2)."""
+        the owner (bf16 communication, gate before fc2).
+        remat (memmodel.cpp:25-31, main.cpp `--no-remat`): True = selective
+        rematerialisation, fc2_in recomputed in backward (the reference
+        default); False = the forward's fc2_in is kept and reused."""
         cfg = _Cfg(tokens_per_rank, hidden, ffn_hidden, num_experts, top_k, ep_size, rank,
                    float(capacity_factor), GATE_ORDERS[gate_order],
                    {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}[comm_format], EP_PATTERNS[ep_pattern],
-                   {"learned": 0, "injected": 1}[route_mode], int(bool(ffn_norm)), float(norm_eps))
+                   {"learned": 0, "injected": 1}[route_mode], int(bool(ffn_norm)), float(norm_eps),
+                   int(not remat))
         self.norm = bool(ffn_norm)
         self.cfg = cfg
         self.Tr, self.h, self.f, self.E, self.k = tokens_per_rank, hidden, ffn_hidden, num_experts, top_k

@@ -235,3 +235,28 @@ def test_protocol_assertions_single_gpu(monkeypatch):
             L.forward(x.cuda())
             L.backward(dy)
         L.status()
+
+
+@pytest.mark.parametrize("gate_order", ["before_fc2_in", "after_fc2_out"])
+def test_no_remat_matches_remat_bit_exact(gate_order):
+    """RematPolicy::off (`--no-remat`, memmodel.cpp:25-31): the forward's fc2_in
+    feeds the fc2 weight gradient instead of the fc2-dgrad epilogue's recompute;
+    both hold the same bf16 values, so every output is bit-identical."""
+    from paper_2505_11432_b200.layer import MoELayer
+    T, h, f, E, k = 512, 512, 768, 8, 2
+    g = torch.Generator().manual_seed(5)
+    x = (torch.randn(T, h, generator=g) * 0.5).bfloat16().cuda()
+    dy = (torch.randn(T, h, generator=g) * 0.1).bfloat16().cuda()
+    w1 = (torch.randn(E, 2 * f, h, generator=g) / h ** 0.5).bfloat16().cuda()
+    w2 = (torch.randn(E, h, f, generator=g) / f ** 0.5).bfloat16().cuda()
+    wr = (torch.randn(E, h, generator=g) / h ** 0.5).bfloat16().cuda()
+    outs = []
+    for remat in (True, False):
+        L = MoELayer(T, h, f, E, k, gate_order=gate_order, remat=remat)
+        L.set_weights(w1, w2, wr)
+        y = L.forward(x)
+        res = L.backward(dy)
+        L.status()
+        outs.append([y.clone()] + [t.clone() for t in res])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
