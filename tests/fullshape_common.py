@@ -74,11 +74,29 @@ def zipf_routing(golden_dir, T, k):
     return ex, gt
 
 
-def sample(T, f, n_tok=64, n_col=8):
+def sample(T, f, n_tok=64, n_col=8, dropped=None):
+    """Sampled tokens and intermediate columns. With capacity drops the tokens
+    are drawn from the kept ones (a dropped token's outputs are exact zeros,
+    checked over all of them by check_dropped_zero), so the numeric sample keeps
+    its size whatever the drop rate."""
     rng = np.random.default_rng(7)
-    toks = np.unique(np.concatenate([[0, T - 1], rng.choice(T, n_tok, replace=False)]))
+    if dropped is None:
+        toks = np.unique(np.concatenate([[0, T - 1], rng.choice(T, n_tok, replace=False)]))
+    else:
+        pool = np.flatnonzero(np.asarray(dropped) == 0)
+        toks = np.unique(np.concatenate([pool[:1], pool[-1:], rng.choice(pool, min(n_tok, pool.size), replace=False)]))
     cols = np.sort(rng.choice(f, n_col, replace=False))
     return toks, cols
+
+
+def check_dropped_zero(dropped, y, dx, dgates):
+    """Every dropped token (routing.cpp:113-131) contributes nothing: its y and
+    dx rows and its dgates are exactly zero."""
+    d = np.asarray(dropped) != 0
+    assert not np.any(y[d]), "a dropped token has a non-zero output row"
+    assert not np.any(dx[d]), "a dropped token has a non-zero dx row"
+    assert not np.any(dgates[d]), "a dropped token has non-zero dgates"
+    return int(d.sum())
 
 
 def check_routing(P, c, ex, gt, dr, lg_all, toks, x, wr, n, Tr):

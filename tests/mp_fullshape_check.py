@@ -21,7 +21,8 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-from fullshape_common import CONFIGS, check_routing, dense_errors, make_inputs, sample, wgrad_cols, zipf_routing  # noqa: E402
+from fullshape_common import (CONFIGS, check_dropped_zero, check_routing, dense_errors, make_inputs,  # noqa: E402
+                              sample, wgrad_cols, zipf_routing)
 
 
 def main():
@@ -60,7 +61,7 @@ def main():
         assert (P.orc_capacity_drop(ex, E, n, c["cf"]) == dr).all(), "capacity drops differ from the oracle"
     else:
         assert dr.sum() == 0
-    toks, cols = sample(T, f, n_col=4)
+    toks, cols = sample(T, f, n_col=4, dropped=dr if c.get("cf", 0.0) > 0 else None)
 
     def gather(t):
         out = [torch.empty_like(t) for _ in range(n)]
@@ -91,6 +92,8 @@ def main():
     assert flag.item() == 0, "a rank's scatter map differs from the oracle"
     if rank == 0:
         errs = {}
+        if c.get("cf", 0.0) > 0:
+            check_dropped_zero(dr, Y, DX, DG)
         if lerr is not None:
             errs["logits"] = lerr
             assert lerr < 1e-4, errs
