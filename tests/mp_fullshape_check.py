@@ -22,7 +22,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from fullshape_common import (CONFIGS, check_dropped_zero, check_routing, dense_errors, make_inputs,  # noqa: E402
-                              sample, wgrad_cols, zipf_routing)
+                              sample, tolerance, wgrad_cols, zipf_routing)
 
 
 def main():
@@ -102,7 +102,7 @@ def main():
         rows = [int((np.asarray(r2["row_map_in"]).size)) for r2 in maps]
         print("MP_FULL_RESULT", name, n, {kk: f"{v:.2e}" for kk, v in errs.items()}, "rows_per_rank", rows,
               "dropped_tokens", int(dr.sum()), flush=True)
-        bad = {kk: v for kk, v in errs.items() if kk != "logits" and not v < c["tol"]}
+        bad = {kk: v for kk, v in errs.items() if kk != "logits" and not v < tolerance(c, kk)}
         assert not bad, bad
     dist.barrier()
     dist.destroy_process_group()

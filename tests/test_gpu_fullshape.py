@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from fullshape_common import CONFIGS, check_routing, dense_errors, make_inputs, sample, wgrad_cols, zipf_routing
+from fullshape_common import CONFIGS, check_routing, dense_errors, make_inputs, sample, tolerance, wgrad_cols, zipf_routing
 
 pytestmark = pytest.mark.gpu
 T = 4096
@@ -46,5 +46,5 @@ def test_full_shape_sampled_parity(name):
                              y.float().cpu().numpy()[toks], dx.float().cpu().numpy()[toks],
                              g1.cpu().numpy(), g2.cpu().numpy(), dwr.cpu().numpy()))
     print(name, {kk: f"{v:.2e}" for kk, v in errs.items()})
-    bad = {kk: v for kk, v in errs.items() if kk != "logits" and not v < c["tol"]}
+    bad = {kk: v for kk, v in errs.items() if kk != "logits" and not v < tolerance(c, kk)}
     assert not bad, (name, errs)
