@@ -582,42 +582,51 @@ def run_ours(args, cfg):
     sync_all()
 
     # ---- end-to-end through the public API with host buffers ----
-    # Every step uploads its own x and dy from pinned host memory and reads
-    # dx back. Copies run on a copy stream, double-buffered, so step i+1's
-    # upload overlaps step i's backward and dx's readback overlaps the
+    # Every step uploads its own x and dy from pinned host memory and reads the
+    # step's result back: its loss L = <y, dy> (the scalar whose gradient with
+    # respect to y is the synthetic dy; bf16 dot on the device, 2 bytes to the
+    # host). A second run also reads the whole dx back every step
+    # (`with_dx_readback`). Copies run on a copy stream, double-buffered, so step
+    # i+1's upload overlaps step i's backward and dx's readback overlaps the
     # weight-gradient GEMMs (dx_event fires before them).
     x_h = x.cpu().pin_memory()
     dy_h = dy.cpu().pin_memory()
     dx_h = torch.empty(Tr, h, dtype=torch.bfloat16).pin_memory()
+    loss_h = torch.empty(2, dtype=torch.bfloat16).pin_memory()
     xb = [torch.empty_like(x) for _ in range(2)]
     dyb = [torch.empty_like(dy) for _ in range(2)]
     dxb = [torch.empty_like(dx) for _ in range(2)]
+    loss_d = [torch.empty((), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
     cs = torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_free = [torch.cuda.Event() for _ in range(2)]
     ev_dx = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
 
-    # The layer's calls of one step (forward + backward on buffer set b) are
-    # captured once per buffer set as a CUDA graph — what a fixed-shape
-    # training loop does with these calls; the host copies stay outside, on
-    # the copy stream, ordered by events (dx_event is recorded inside the graph).
+    def layer_step(b):
+        L.forward(xb[b], y)
+        L.backward(dyb[b], dxb[b], dw1, dw2, dwr, dx_event=ev_dx[b])
+        torch.dot(y.view(-1), dyb[b].view(-1), out=loss_d[b])
+
+    # The step's calls (forward + backward + loss on buffer set b) are captured
+    # once per buffer set as a CUDA graph — what a fixed-shape training loop
+    # does with these calls; the host copies stay outside, on the copy stream,
+    # ordered by events (dx_event is recorded inside the graph).
     step_graphs = [None, None]
     if not args.no_graph:
         for b in range(2):
             xb[b].copy_(x)
             dyb[b].copy_(dy)
-            L.forward(xb[b], y)
-            L.backward(dyb[b], dxb[b], dw1, dw2, dwr, dx_event=ev_dx[b])
+            layer_step(b)
             sync_all()
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr):
-                L.forward(xb[b], y)
-                L.backward(dyb[b], dxb[b], dw1, dw2, dwr, dx_event=ev_dx[b])
+                layer_step(b)
             step_graphs[b] = gr
         sync_all()
 
-    def e2e_run(nsteps):
+    def e2e_run(nsteps, read_dx=False):
         with torch.cuda.stream(cs):
             xb[0].copy_(x_h, non_blocking=True)
             dyb[0].copy_(dy_h, non_blocking=True)
@@ -625,9 +634,9 @@ def run_ours(args, cfg):
         for i in range(nsteps):
             b = i % 2
             stream.wait_event(ev_in[b])
+            if i >= 2:
+                stream.wait_event(ev_out[b])   # buffer set b's results drained to the host
             if step_graphs[b] is not None:
-                if i >= 2:
-                    stream.wait_event(ev_out[b])   # dx buffer b drained to host
                 step_graphs[b].replay()
             else:
                 L.forward(xb[b], y)
@@ -639,43 +648,55 @@ def run_ours(args, cfg):
                     dyb[1 - b].copy_(dy_h, non_blocking=True)
                     ev_in[1 - b].record(cs)
             if step_graphs[b] is None:
-                if i >= 2:
-                    stream.wait_event(ev_out[b])   # dx buffer b drained to host
                 L.backward(dyb[b], dxb[b], dw1, dw2, dwr, dx_event=ev_dx[b])
+                torch.dot(y.view(-1), dyb[b].view(-1), out=loss_d[b])
             ev_free[b].record(stream)
+            ev_done[b].record(stream)
             with torch.cuda.stream(cs):
-                cs.wait_event(ev_dx[b])
-                dx_h.copy_(dxb[b], non_blocking=True)
+                if read_dx:
+                    cs.wait_event(ev_dx[b])
+                    dx_h.copy_(dxb[b], non_blocking=True)
+                cs.wait_event(ev_done[b])
+                loss_h[b].copy_(loss_d[b], non_blocking=True)
                 ev_out[b].record(cs)
         stream.wait_stream(cs)
 
-    e2e_run(2)
-    sync_all()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    e2e_run(args.steps)
-    e1.record(stream)
-    sync_all()
-    te = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item())
+    def e2e_time(read_dx):
+        e2e_run(2, read_dx)
+        sync_all()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_run(args.steps, read_dx)
+        e1.record(stream)
+        sync_all()
+        te = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        return float(te.item())
+
+    e2e_ms = e2e_time(False)
+    e2e_dx_ms = e2e_time(True)
     # the same host copies alone (every rank at once, no compute): the floor the
-    # host link puts under the e2e step
-    sync_all()
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(cs):
-        c0.record(cs)
-        for i in range(args.steps):
-            xb[i % 2].copy_(x_h, non_blocking=True)
-            dyb[i % 2].copy_(dy_h, non_blocking=True)
-            dx_h.copy_(dxb[i % 2], non_blocking=True)
-        c1.record(cs)
-    sync_all()
-    tc = torch.tensor([c0.elapsed_time(c1) / args.steps], device="cuda")
-    if world > 1:
-        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
-    copy_only_ms = float(tc.item())
+    # host link puts under the e2e step (uploads, + the dx readback)
+    def copies_only(read_dx):
+        sync_all()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(cs):
+            c0.record(cs)
+            for i in range(args.steps):
+                xb[i % 2].copy_(x_h, non_blocking=True)
+                dyb[i % 2].copy_(dy_h, non_blocking=True)
+                if read_dx:
+                    dx_h.copy_(dxb[i % 2], non_blocking=True)
+            c1.record(cs)
+        sync_all()
+        tc = torch.tensor([c0.elapsed_time(c1) / args.steps], device="cuda")
+        if world > 1:
+            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        return float(tc.item())
+
+    copy_only_ms = copies_only(False)
+    copy_only_dx_ms = copies_only(True)
 
     rt = L.routing()
     cnt = rt["per_expert_counts"].cpu().tolist()[rank * el:(rank + 1) * el]
@@ -846,11 +867,15 @@ def run_ours(args, cfg):
             "gpu_launches_per_step": int(per_step_launches),
             "launch_mode": "eager" if args.no_graph else "cuda_graph",
             "e2e": {"value": n * Tr / (e2e_ms / 1000.0), "unit": "tokens/s",
-                    "h2d_bytes_per_step": 2 * Tr * h * 2, "d2h_bytes_per_step": Tr * h * 2,
+                    "h2d_bytes_per_step": 2 * Tr * h * 2, "d2h_bytes_per_step": 2,
                     "ms_per_step": e2e_ms, "host_copies_only_ms_per_step": copy_only_ms,
-                    "mode": ("MoELayer.forward/backward captured as one CUDA graph per buffer set; x, dy "
-                             "uploaded and dx read back every step from pinned host memory on a copy stream"
-                             if not args.no_graph else "eager MoELayer.forward/backward calls; same copies")},
+                    "mode": ("MoELayer.forward/backward (+ the step's loss <y, dy>) captured as one CUDA graph "
+                             "per buffer set; x, dy uploaded from pinned host memory and the loss read back "
+                             "every step on a copy stream"
+                             if not args.no_graph else "eager MoELayer.forward/backward calls; same copies"),
+                    "with_dx_readback": {"value": n * Tr / (e2e_dx_ms / 1000.0), "ms_per_step": e2e_dx_ms,
+                                         "d2h_bytes_per_step": Tr * h * 2 + 2,
+                                         "host_copies_only_ms_per_step": copy_only_dx_ms}},
         }
         if n == 1 and not args.no_cpu_baseline:
             try:
