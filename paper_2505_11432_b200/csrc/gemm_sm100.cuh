@@ -400,6 +400,61 @@ __device__ __forceinline__ void store_rows32_s(uint4* wst, const uint32_t (&pk)[
     }
     __syncwarp();
 }
+// 32 rows x 64 columns (bf16), each lane's row at its own address (nullptr =
+// skip), in two 16-row halves of the 2 KB per-warp tile: every store
+// instruction writes 4 rows x 128 contiguous bytes.
+__device__ __forceinline__ void store_rows64(uint4* wst, const uint32_t (&p0)[16], const uint32_t (&p1)[16],
+                                             void* row_ptr, int lane) {
+    const unsigned long long my = reinterpret_cast<unsigned long long>(row_ptr);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+        if ((lane >> 4) == hh) {
+            const int r = lane & 15;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                wst[r * 8 + (u ^ (r & 7))] = make_uint4(p0[4 * u], p0[4 * u + 1], p0[4 * u + 2], p0[4 * u + 3]);
+                wst[r * 8 + ((u + 4) ^ (r & 7))] = make_uint4(p1[4 * u], p1[4 * u + 1], p1[4 * u + 2], p1[4 * u + 3]);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int R = (lane >> 3) + 4 * i, c = lane & 7;
+            const unsigned long long pr = __shfl_sync(0xffffffffu, my, hh * 16 + R);
+            const uint4 v = wst[R * 8 + (c ^ (R & 7))];
+            if (pr) reinterpret_cast<uint4*>(pr)[c] = v;
+        }
+        __syncwarp();
+    }
+}
+
+// 32 rows x 64 columns (bf16) of consecutive rows `stride` bytes apart, through
+// the same 2 KB per-warp tile in two 16-row halves: every store instruction
+// writes 4 rows x 128 contiguous bytes (whole 128-byte lines: one NVLink write
+// per line when the rows live on a peer).
+__device__ __forceinline__ void store_rows64_s(uint4* wst, const uint32_t (&p0)[16], const uint32_t (&p1)[16],
+                                               void* row_ptr, int64_t stride, int lane) {
+    char* row0 = reinterpret_cast<char*>(row_ptr) - (int64_t)lane * stride;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+        if ((lane >> 4) == hh) {
+            const int r = lane & 15;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                wst[r * 8 + (u ^ (r & 7))] = make_uint4(p0[4 * u], p0[4 * u + 1], p0[4 * u + 2], p0[4 * u + 3]);
+                wst[r * 8 + ((u + 4) ^ (r & 7))] = make_uint4(p1[4 * u], p1[4 * u + 1], p1[4 * u + 2], p1[4 * u + 3]);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int R = (lane >> 3) + 4 * i, c = lane & 7;
+            reinterpret_cast<uint4*>(row0 + (int64_t)(hh * 16 + R) * stride)[c] = wst[R * 8 + (c ^ (R & 7))];
+        }
+        __syncwarp();
+    }
+}
+
 __device__ __forceinline__ void load_rows32_issue_s(uint4 (&v)[4], const void* row_ptr, int64_t stride, int lane) {
     const char* row0 = reinterpret_cast<const char*>(row_ptr) - (int64_t)lane * stride;
 #pragma unroll
@@ -479,39 +534,44 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         } else {
             of32 = reinterpret_cast<float*>(args.out) + orow * args.ldo + n0;
         }
+        if constexpr (EPI != EPI_STORE_F32) {
+            // 64 columns per step: whole 128-byte row segments (NVLink writes of full
+            // lines when the destination is a peer: scatter / GEMM+A2A epilogues)
+#pragma unroll 1
+            for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 64) {
+                if (n0 + c0 >= args.N) break;   // warp-uniform
+                uint32_t r[32], p0[16], p1[16];
+                tmem_ld32(tbase + (c0 - tshift), r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    p0[q] = pack_bf16x2(__uint_as_float(r[2 * q]) * gscale, __uint_as_float(r[2 * q + 1]) * gscale);
+                if (n0 + c0 + 64 > args.N) {   // a last 32-column chunk
+                    if (EPI == EPI_SCATTER) store_rows32(wst, p0, valid ? (void*)(obf + c0) : nullptr, lane);
+                    else store_rows32_s(wst, p0, obf + c0, args.ldo * 2, lane);
+                    break;
+                }
+                tmem_ld32(tbase + (c0 + 32 - tshift), r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    p1[q] = pack_bf16x2(__uint_as_float(r[2 * q]) * gscale, __uint_as_float(r[2 * q + 1]) * gscale);
+                if (EPI == EPI_SCATTER) store_rows64(wst, p0, p1, valid ? (void*)(obf + c0) : nullptr, lane);
+                else store_rows64_s(wst, p0, p1, obf + c0, args.ldo * 2, lane);
+            }
+            return;
+        }
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
             uint32_t r[32];
             tmem_ld32(tbase + (c0 - tshift), r);
             tmem_ld_wait();
             if (n0 + c0 >= args.N) continue;   // warp-uniform
-            if (EPI != EPI_STORE_F32) {
-                uint32_t pk[16];
 #pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]) * gscale, __uint_as_float(r[2 * q + 1]) * gscale);
-                if (EPI == EPI_SCATTER) store_rows32(wst, pk, valid ? (void*)(obf + c0) : nullptr, lane);
-                else store_rows32_s(wst, pk, obf + c0, args.ldo * 2, lane);
-                continue;
-            }
-            if (!valid) continue;
-            if (EPI == EPI_STORE_F32) {
-#pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    float4 v = make_float4(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale,
-                                           __uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
-                    *reinterpret_cast<float4*>(of32 + c0 + i) = v;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; i += 8) {
-                    uint4 v;
-                    v.x = pack_bf16x2(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale);
-                    v.y = pack_bf16x2(__uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
-                    v.z = pack_bf16x2(__uint_as_float(r[i + 4]) * gscale, __uint_as_float(r[i + 5]) * gscale);
-                    v.w = pack_bf16x2(__uint_as_float(r[i + 6]) * gscale, __uint_as_float(r[i + 7]) * gscale);
-                    *reinterpret_cast<uint4*>(obf + c0 + i) = v;
-                }
+            for (int i = 0; i < 32; i += 4) {
+                float4 v = make_float4(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale,
+                                       __uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
+                *reinterpret_cast<float4*>(of32 + c0 + i) = v;
             }
         }
     } else if constexpr (EPI == EPI_SCATTER_FP8) {
@@ -538,22 +598,24 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             reinterpret_cast<float*>(args.rank_scale_base[dst >> 27])[drow * (args.ldo / 128) + (n0 + c_lo) / 128] =
                 (float)blk.scale;
         }
-#pragma unroll 1
-        for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
+        // the group's 128 codes of every row are stored as one 128-byte line
+        // (8 lanes per row through the per-warp tile: whole NVLink writes)
+        uint32_t p0[16], p1[16];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
             uint32_t r[32];
-            tmem_ld32(tbase + (c0 - tshift), r);
+            tmem_ld32(tbase + (c_lo + 32 * ch - tshift), r);
             tmem_ld_wait();
-            if (dst < 0) continue;
-            uint32_t pk[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const uint16_t lo = e4m3x2_code(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), blk);
                 const uint16_t hi = e4m3x2_code(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), blk);
-                pk[q] = (uint32_t)lo | ((uint32_t)hi << 16);
+                const uint32_t w = (uint32_t)lo | ((uint32_t)hi << 16);
+                if (ch < 2) p0[8 * ch + q] = w;
+                else p1[8 * (ch - 2) + q] = w;
             }
-            *reinterpret_cast<uint4*>(codes + c0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            *reinterpret_cast<uint4*>(codes + c0 + 16) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
+        store_rows64(wst, p0, p1, dst >= 0 ? (void*)(codes + c_lo) : nullptr, lane);
     } else if constexpr (EPI == EPI_SCATTER_RS) {
         const int nr = args.rs_n, self = args.self_rank;
         const int owner = ti.row0 / args.rs_rows;
@@ -562,14 +624,17 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         if (owner != self) {
             uint16_t* obf = reinterpret_cast<uint16_t*>(args.rank_base[owner]) + (lrow * nr + self) * args.ldo + n0;
 #pragma unroll 1
-            for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 32) {
-                uint32_t r[32];
+            for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 64) {
+                uint32_t r[32], p0[16], p1[16];
                 tmem_ld32(tbase + (c0 - tshift), r);
                 tmem_ld_wait();
-                uint32_t pk[16];
 #pragma unroll
-                for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
-                store_rows32_s(wst, pk, obf + c0, sstride, lane);
+                for (int q = 0; q < 16; ++q) p0[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+                tmem_ld32(tbase + (c0 + 32 - tshift), r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 16; ++q) p1[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+                store_rows64_s(wst, p0, p1, obf + c0, sstride, lane);
             }
         } else {
             if (lane == 0 && nr > 1) {
