@@ -259,6 +259,7 @@ moe_status moe_attn_gemm_rs(moe_attn* A, const uint16_t* d_o, uint16_t* d_y_shar
     a.ldo = A->h;
     a.row_dst = A->row_dst;
     a.rank_base = reinterpret_cast<void* const*>(A->tab + A->n);
+    a.wide_rows = A->n > 1;
     a.err = A->err;
     if (A->rs_fused) {
         // owners finished reading the previous call's staging; bumps the call count

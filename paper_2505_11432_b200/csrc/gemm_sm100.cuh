@@ -129,6 +129,7 @@ struct GemmArgs {
     uint16_t* rs_out;
     int rs_rows, rs_n;
     int rs_tile_m, rs_tile_warps;   // rows per tile, epilogue warps per tile (both CTAs)
+    int wide_rows;                  // SCATTER / GEMM+A2A STORE: rows mostly go to peers -> 128-byte lines
     int rs_order, rs_delay;         // 1: fused GEMM-RS tile order (decode_tile), own tiles of a
                                     // column rs_delay blocks after the peers'
 };
@@ -534,9 +535,12 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
         } else {
             of32 = reinterpret_cast<float*>(args.out) + orow * args.ldo + n0;
         }
-        if constexpr (EPI != EPI_STORE_F32) {
-            // 64 columns per step: whole 128-byte row segments (NVLink writes of full
-            // lines when the destination is a peer: scatter / GEMM+A2A epilogues)
+        // peer-bound rows (scatter, GEMM + A2A with peers: args.wide_rows): 64 columns
+        // per step, whole 128-byte row lines = full NVLink writes. Local stores keep
+        // 32-column steps: the half-warp staging of the wide path measured 4-6% slower
+        // on the short-K wgrad tiles and 1-3% on the N = 1 scatter GEMMs.
+        if ((EPI == EPI_SCATTER || (EPI == EPI_STORE_BF16 && !K_GROUPED && args.col_owner_cols > 0)) &&
+            args.wide_rows) {
 #pragma unroll 1
             for (int c0 = c_lo; c0 < c_lo + HALF; c0 += 64) {
                 if (n0 + c0 >= args.N) break;   // warp-uniform
@@ -567,11 +571,20 @@ __device__ __forceinline__ void epilogue_rows(const GemmArgs& args, const TileIn
             tmem_ld32(tbase + (c0 - tshift), r);
             tmem_ld_wait();
             if (n0 + c0 >= args.N) continue;   // warp-uniform
+            if constexpr (EPI != EPI_STORE_F32) {
+                uint32_t pk[16];
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                float4 v = make_float4(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale,
-                                       __uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
-                *reinterpret_cast<float4*>(of32 + c0 + i) = v;
+                for (int q = 0; q < 16; ++q)
+                    pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]) * gscale, __uint_as_float(r[2 * q + 1]) * gscale);
+                if (EPI == EPI_SCATTER) store_rows32(wst, pk, valid ? (void*)(obf + c0) : nullptr, lane);
+                else store_rows32_s(wst, pk, obf + c0, args.ldo * 2, lane);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    float4 v = make_float4(__uint_as_float(r[i]) * gscale, __uint_as_float(r[i + 1]) * gscale,
+                                           __uint_as_float(r[i + 2]) * gscale, __uint_as_float(r[i + 3]) * gscale);
+                    *reinterpret_cast<float4*>(of32 + c0 + i) = v;
+                }
             }
         }
     } else if constexpr (EPI == EPI_SCATTER_FP8) {

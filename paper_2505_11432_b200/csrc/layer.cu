@@ -783,6 +783,7 @@ static moe_status fwd_fc2_combine(moe_layer* L, uint16_t* d_y, cudaStream_t s) {
         } else {
             a.row_dst = L->row_dst;
             a.rank_base = L->fp8 ? L->tab<void>(F_STAGE8) : L->tab<void>(F_STAGE);
+            a.wide_rows = L->n > 1;
             a.rank_scale_base = L->tab<void>(F_SSC);
             MOE_TRY(gemm_launch(L->p_fc2, a, s));
         }
@@ -921,6 +922,7 @@ moe_status moe_layer_backward_ex(moe_layer* L, const uint16_t* d_dy, uint16_t* d
         } else {
             a.row_dst = L->row_dst;
             a.rank_base = L->fp8 ? L->tab<void>(F_DSTAGE8) : L->tab<void>(F_DSTAGE);
+            a.wide_rows = L->n > 1;
             a.rank_scale_base = L->tab<void>(F_DSSC);
             MOE_TRY(gemm_launch(L->p_fc1_dgrad, a, s));
         }

@@ -192,6 +192,7 @@ moe_status moe_ulysses_qkv_a2a(moe_ulysses* U, const uint16_t* d_x_shard, moe_st
     a.K = (int)U->h;
     a.ldo = U->cpo;
     a.col_owner_cols = (int)U->cpo;
+    a.wide_rows = U->n > 1;
     a.owner_row0 = (int)(U->rank * U->sr);
     a.rank_base = reinterpret_cast<void* const*>(U->tab);
     MOE_TRY(gemm_launch(p, a, s));
