@@ -46,3 +46,34 @@ def test_product_has_no_cpu_fallback():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert "pyoracle" not in txt and "moe_oracle" not in txt, fn
+
+
+def _c_layout(struct_name, fields):
+    """sizeof and offsetof of a header struct, from a C program compiled here."""
+    import shutil
+    import subprocess
+    import tempfile
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    body = "".join(f'printf("%zu\\n", offsetof({struct_name}, {f}));' for f in fields)
+    src = ("#include <stddef.h>\n#include <stdio.h>\n#include \"moe_b200.h\"\n"
+           f"int main(void) {{ printf(\"%zu\\n\", sizeof({struct_name})); {body} return 0; }}\n")
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "layout.c")
+        exe = os.path.join(d, "layout")
+        open(c, "w").write(src)
+        subprocess.run([cc, "-I", os.path.join(ROOT, "include"), "-I/usr/local/cuda/include", c, "-o", exe],
+                       check=True, capture_output=True)
+        return [int(v) for v in subprocess.run([exe], check=True, capture_output=True, text=True).stdout.split()]
+
+
+def test_python_structs_match_the_c_header_layout():
+    """The ctypes mirrors of the C-ABI structs (moe_layer_config, the routing
+    view) have the header's size and field offsets."""
+    from paper_2505_11432_b200.layer import _Cfg, _RoutingView
+    for cls, name in ((_Cfg, "moe_layer_config"), (_RoutingView, "moe_layer_routing_view")):
+        fields = [f for f, _ in cls._fields_]
+        got = _c_layout(name, fields)
+        want = [ctypes.sizeof(cls)] + [getattr(cls, f).offset for f in fields]
+        assert got == want, (name, got, want)
