@@ -227,6 +227,15 @@ moe_status moe_attn_ag_gemm(moe_attn* A, const uint16_t* d_x_shard, uint16_t* d_
     a.out = d_qkv;
     a.ldo = A->nq;
     a.m_chunk = 4;  // first wave waits for 4 row blocks, not the whole gather
+    {
+        // a partial last wave of at most half the CTA pairs runs as M = 128 pair tiles
+        // (TP = 4: 320 tiles = 4 waves + 24 -> the last 24 become 48 half tiles)
+        const int units = kNumSMs / A->cg;
+        const int tiles = (int)(A->s / (128 * A->cg)) * (int)((A->nq + A->p_qkv.bn - 1) / A->p_qkv.bn);
+        const int rem = tiles % units;
+        static const bool no_split = getenv("MOE_ATTN_NO_TAIL_SPLIT") != nullptr;
+        if (A->cg == 2 && rem > 0 && 2 * rem <= units && !no_split) a.split_last = rem;
+    }
     // start on this rank's own shard, then the next rank's (rotation): the first
     // wave needs no peer rows and every rank pulls from a different peer at a time
     a.m_rot = (int)(A->rank * A->sr / (128 * A->cg));

@@ -130,6 +130,8 @@ struct GemmArgs {
     int rs_rows, rs_n;
     int rs_tile_m, rs_tile_warps;   // rows per tile, epilogue warps per tile (both CTAs)
     int wide_rows;                  // SCATTER / GEMM+A2A STORE: rows mostly go to peers -> 128-byte lines
+    int split_last;                 // M-grouped, one group, CTA pairs: the last split_last tiles run as
+                                    // 2 x M = 128 pair tiles each (decode_tile)
     int rs_order, rs_delay;         // 1: fused GEMM-RS tile order (decode_tile), own tiles of a
                                     // column rs_delay blocks after the peers'
 };
@@ -163,6 +165,15 @@ struct TileInfo {
 template <int TILE_M, bool K_GROUPED>
 __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const int* row_off,
                                                 const int* kb, const GemmArgs& a, int G, int n_tiles) {
+    // the last split_last pair tiles of the sequence run as two M = 128 pair tiles
+    // each (rows row0 and row0 + 128): a partial last wave of full tiles becomes
+    // a shorter wave of half tiles (the host only sets it when it fits one wave)
+    int split_half = -1;
+    if (!K_GROUPED && TILE_M == 256 && a.split_last > 0 && t >= prefix[G] - a.split_last) {
+        const int u = t - (prefix[G] - a.split_last);
+        t = prefix[G] - a.split_last + (u >> 1);
+        split_half = u & 1;
+    }
     int lo = 0, hi = G - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
@@ -212,6 +223,10 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* prefix, const 
         ti.kblocks = (a.K + 63) / 64;
         ti.row0 = row_off[lo] + ti.m * TILE_M;
         ti.half_tile = TILE_M == 256 && ti.m * TILE_M + TILE_M > rows;
+        if (split_half >= 0) {
+            ti.row0 += split_half * 128;
+            ti.half_tile = 1;
+        }
     } else {
         // n fastest: a wave of tiles shares a few A panels and streams all
         // of B's (small) contraction panel from L2
@@ -1083,7 +1098,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS + (DISPATCH ? 32 * Ge
     if (CG == 2) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int total_tiles = prefix[G];
+    const int total_tiles = prefix[G] + (K_GROUPED ? 0 : args.split_last);
     // dynamic for M-grouped GEMMs (M = 128 tail tiles and dispatch waits make
     // tile costs uneven, and a drifting static stride breaks the L2 sharing of
     // weight panels: 2.3x DRAM reads measured); the K-grouped wgrads keep the
