@@ -556,11 +556,12 @@ def run_ours(args, cfg):
     membw = None
     if cfg.get("comm", "bf16") == "bf16" and cfg.get("gate", "before_fc2_in") == "before_fc2_in" \
             and args.ep_pattern == "a2a":
+        fused_default = L.fused_dispatch()
         L.set_fused_dispatch(False)
         L.forward(None, y)
         L.backward(dy, dx, dw1, dw2, dwr)
         pu = L.phase_times()
-        L.set_fused_dispatch(True)
+        L.set_fused_dispatch(fused_default)
         rows_pad = routing_probe_rows(L, rank, el)
         hbm = load_peaks()["hbm"]
         rb = Tr * h * 2 + E * h * 2              # router: x + W_r
@@ -829,6 +830,7 @@ def run_ours(args, cfg):
                        "parallelism": f"ep{n}", "comm_format": cfg.get("comm", "bf16"),
                        "gate_order": cfg.get("gate", "before_fc2_in"), "ep_pattern": args.ep_pattern,
                        "remat": "off" if args.no_remat else "selective",
+                       "dispatch": "fused into fc1 / fc2-dgrad" if L.fused_dispatch() else "separate scatter kernel",
                        "l2": "inputs larger than L2 (expert weights >= 2.8 GB/layer)"},
             "roofline": roof,
             "phases_ms": {kk: round(v, 4) for kk, v in phases.items()},

@@ -305,10 +305,14 @@ moe_status moe_layer_enable_stamps(moe_layer* L, int enable);
 moe_status moe_layer_read_stamps(moe_layer* L, uint64_t* h_ns, int max_slots, int* n_phases,
                                  const char** names);
 
-/* 1 (default): dispatch (AG + local scatter) fused into the fc1 / fc2-dgrad
- * GEMMs; 0: a separate memory-bound scatter kernel (the reference's unfused
- * operator structure, graph.cpp:276-286; used to measure it). */
+/* 1: dispatch (AG + local scatter) fused into the fc1 / fc2-dgrad GEMMs;
+ * 0: a separate memory-bound scatter kernel (the reference's unfused operator
+ * structure, graph.cpp:276-286). Default: fused when ep_size > 1 or top_k > 2
+ * (and always for FP8 comm, gate after fc2 and ag_rs, which need it); unfused
+ * on one GPU with top-k <= 2, where there are no peer rows to overlap and the
+ * separate copy is small (measured faster). */
 moe_status moe_layer_set_fused_dispatch(moe_layer* L, int fused);
+int moe_layer_get_fused_dispatch(moe_layer* L);
 
 /* Non-zero if a cross-GPU flag wait of this layer timed out (synchronous). */
 int moe_layer_error_flag(moe_layer* L);

@@ -533,9 +533,20 @@ moe_status moe_layer_create(const moe_layer_config* cfg, moe_layer** out) {
     }
     *L->err_host = 0;
     cudaMemset(L->epoch_dev, 0, sizeof(uint32_t));
-    // the unfused (reference-structure) dispatch path is kept for A/B runs;
-    // gate-after-fc2 backward needs the fused path's row scaling
-    L->fused_dispatch = getenv("MOE_UNFUSED_DISPATCH") == nullptr || L->gate_after || L->fp8 || L->ag;
+    // Dispatch fused into fc1 / fc2-dgrad (comm warps) when there are peer rows to
+    // overlap or the permuted copy is large: on one GPU with top-2 routing the
+    // separate scatter kernel + plain GEMMs measured 0.06 ms per Mixtral step
+    // faster (fc1 1.46 -> 1.41 ms, fc2-dgrad 0.83 -> 0.79 ms for 0.035 ms of
+    // scatter kernels), while with top-8 (DeepSeek) the two 1.1 GB scatter passes
+    // cost more than the comm warps (17.5 -> 17.9 ms). Gate-after-fc2 backward,
+    // FP8 comm and ag_rs need the fused path. MOE_FUSED_DISPATCH=1 /
+    // MOE_UNFUSED_DISPATCH=1 override.
+    {
+        bool fused = L->n > 1 || L->k > 2;
+        if (getenv("MOE_FUSED_DISPATCH")) fused = true;
+        if (getenv("MOE_UNFUSED_DISPATCH")) fused = false;
+        L->fused_dispatch = fused || L->gate_after || L->fp8 || L->ag;
+    }
     // on by default (DeepSeek shape, EP = 4: 9.17 -> 8.93 ms per step with the
     // dynamic tile schedule; Mixtral EP = 4 unchanged); MOE_NO_DISPATCH_DEDUP=1 off
     L->dedup = L->n > 1 && L->k > 1 && L->el > 1 && !L->ag && getenv("MOE_NO_DISPATCH_DEDUP") == nullptr;
@@ -1117,6 +1128,8 @@ moe_status moe_layer_set_fused_dispatch(moe_layer* L, int fused) {
     L->fused_dispatch = fused != 0;
     return MOE_OK;
 }
+
+int moe_layer_get_fused_dispatch(moe_layer* L) { return L && L->fused_dispatch ? 1 : 0; }
 
 moe_status moe_layer_set_comm_mode(moe_layer* L, int compute_only) {
     MOE_CHECK_ARG(L, "null argument");

@@ -236,6 +236,9 @@ class MoELayer:
     def set_fused_dispatch(self, on: bool):
         check(lib().moe_layer_set_fused_dispatch(self._h, int(bool(on))))
 
+    def fused_dispatch(self) -> bool:
+        return bool(lib().moe_layer_get_fused_dispatch(self._h))
+
     def set_compute_only(self, on: bool):
         """Exposed-comm measurement mode (see moe_layer_set_comm_mode)."""
         check(lib().moe_layer_set_comm_mode(self._h, int(bool(on))))
