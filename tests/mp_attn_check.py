@@ -16,8 +16,8 @@ def main():
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank))))
     from paper_2505_11432_b200.attn import AttnProjections
-    s, h = 1024 * n, 1024
-    nq = 256 * 5 // 2 if n == 1 else 320  # any multiple of 64
+    s, h = int(os.environ.get("MP_ATTN_S", 1024 * n)), 1024
+    nq = int(os.environ.get("MP_ATTN_NQ", 256 * 5 // 2 if n == 1 else 320))  # any multiple of 64
     g = torch.Generator().manual_seed(0)
     x = (torch.randn(s, h, generator=g) * 0.5).bfloat16()
     wqkv = (torch.randn(n, nq, h, generator=g) / h ** 0.5).bfloat16()
