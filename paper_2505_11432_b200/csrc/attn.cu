@@ -9,11 +9,13 @@
 //            by block, and the TMA producer waits per block (identity
 //            permutation of the MoE dispatch path, k = 1).
 //   GEMM-RS  y_r[s/n, h] = sum over ranks of (o[s, h/n] . Wout_r[h, h/n]^T)
-//            tiles are taken shard by shard, peers' shards first (rank+1, ...)
-//            and this rank's own shard last. A peer shard's tile is stored to
-//            the owner's staging slot (row, source rank) and counted on the
-//            owner's per-tile counter; an own tile waits for its n-1 counts and
-//            its epilogue sums the n partials in fixed rank order in fp32
+//            tiles run in blocks: block c = the peer shards' tiles of output
+//            column c (shards rank+1, rank+2, ...), then this rank's own tiles
+//            of column c - D (decode_tile, rs_order). A peer shard's tile is
+//            stored to the owner's staging slot (row, source rank) in whole
+//            128-byte lines and counted on the owner's per-tile counter by the
+//            CTA's signal warp; an own tile waits for its n-1 counts and its
+//            epilogue sums the n partials in fixed rank order in fp32
 //            (a2a_fp32 reduction semantics, numerics.cpp:172-192) straight into
 //            y: no trailing barrier, no separate reduce kernel
 //            (MOE_ATTN_RS_UNFUSED=1 at create: staging for every tile, flag
