@@ -24,6 +24,8 @@
 //   warps 2..9    : epilogue, two warps per TMEM lane quarter (each half of the
 //                   columns); TMEM double-buffered so tile i's epilogue
 //                   overlaps tile i+1's MMA.
+//   warps 10..11  : fused dispatch only: comm warps filling the A rows (dispatch_warp)
+//   warp 10       : EPI_SCATTER_RS only: signal warp (per-tile arrival counts at the owner)
 #pragma once
 
 #include <type_traits>
